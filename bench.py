@@ -1,0 +1,345 @@
+#!/usr/bin/env python
+"""bench.py — MPKK (arXiv:1309.4349) throughput on B200.
+
+Metric (BASELINE.json): site-updates/s of Kawasaki MC (one site update = one
+attempted exchange; one sweep = N of them, R11) and HBM GB/s vs
+roofline, at 1/2/4/8 GPUs.
+
+Step (R11): one sampling interval = S=100 MPKK sweeps + one
+observable sample (N_AB energy, composition, acceptance counters, cluster-size
+histogram) read back to the host.
+
+Workload (BASELINE configs[4]): a 65536 x 65536 row slab per GPU (weak
+scaling, global lattice 65536 x 65536*N), omega/kT = 0.6, 50:50, random start.
+The lattice (2 x 512 MiB bit-packed per GPU) is larger than L2 (126 MB), so no
+flush is needed between iterations.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+N>1 runs under torchrun (one rank per GPU, NCCL halo exchange).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "site-updates/sec (Kawasaki MC) and HBM GB/s vs roofline at 1/2/4/8 B200"
+UNIT = "site-updates/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--Lx", type=int, default=65536)
+    p.add_argument("--rows-per-gpu", type=int, default=65536)
+    p.add_argument("--sweeps-per-step", type=int, default=100)
+    p.add_argument("--omega", type=float, default=0.6)
+    p.add_argument("--fraction", type=float, default=0.5)
+    p.add_argument("--seed", type=int, default=20261018)
+    p.add_argument("--T", type=int, default=4, help="MPKK iterations per HBM pass")
+    p.add_argument("--no-ccl", action="store_true", help="skip the cluster histogram in the step")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    return p.parse_args()
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (profiling recipe)."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), float(d.get("sm_max_mhz", 1965.0)), "measured"
+    except Exception:
+        return 6650.0, 1965.0, "fallback"
+
+
+def kernel_counters():
+    """Per-site-update instruction count and DRAM bytes of the pass kernel from
+    the committed ncu capture (profiles/pass_kernel_counters.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "pass_kernel_counters.json")) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------------ CPU baseline
+def cpu_baseline(seconds: float, omega: float, fraction: float, seed: int):
+    """The oracle as it stands (single-threaded C), on a bounded sample."""
+    from oracle import oracle as O
+    Lx = Ly = 1024
+    lat = O.init_random(Lx, Ly, fraction, seed)
+    t0 = time.perf_counter()
+    n = 0
+    while time.perf_counter() - t0 < seconds:
+        O.run(lat, omega, seed, 1, first_sweep=n)
+        n += 1
+    dt = time.perf_counter() - t0
+    return {"value": n * Lx * Ly / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{Lx}x{Ly} lattice, {n} MPKK sweeps, omega={omega}, single thread, "
+                      f"{dt:.1f} s"}
+
+
+def run_reference(a, rank, world):
+    """--impl reference: the oracle on the host cores, bounded steps."""
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    Lx = Ly = 1024
+    lat = O.init_random(Lx, Ly, a.fraction, a.seed)
+    per_step_sweeps = 2
+    for w in range(a.warmup):
+        O.run(lat, a.omega, a.seed, per_step_sweeps, first_sweep=w * per_step_sweeps)
+    t0 = time.perf_counter()
+    for k in range(a.steps):
+        O.run(lat, a.omega, a.seed, per_step_sweeps, first_sweep=(a.warmup + k) * per_step_sweeps)
+        O.n_ab(lat)
+        O.composition(lat)
+        O.cluster_histogram(lat, 1)
+    dt = time.perf_counter() - t0
+    v = a.steps * per_step_sweeps * Lx * Ly / dt
+    out = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * dt / a.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u1",
+        "data": "synthetic",
+        "config": {"workload": f"oracle sample of configs[4]: {Lx}x{Ly}, {per_step_sweeps} sweeps + "
+                               "observables per step", "omega_kT": a.omega, "fraction_A": a.fraction},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"{Lx}x{Ly}, {per_step_sweeps} sweeps/step, single thread"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+# ------------------------------------------------------------------------------ ours
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(a.gpus)))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        run_reference(a, rank, world if world > 1 else 1)
+        return
+    import torch
+    assert torch.cuda.is_available(), "bench.py needs a CUDA device"
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1309_4349_b200 import build as B
+    if rank == 0:
+        B.build()
+    if dist:
+        dist.barrier()
+    from paper_1309_4349_b200 import kk
+    from paper_1309_4349_b200 import distributed as D
+
+    rows = a.rows_per_gpu
+    Lx, Ly = a.Lx, rows * world
+    stream = torch.cuda.current_stream()
+    sim = D.make_simulation(Lx, Ly, a.fraction, a.omega, a.seed, T=a.T, world=world, rank=rank,
+                            device=local, stream=stream)
+    N_local = Lx * rows
+    passes_per_sweep = 16 // a.T
+
+    pass_events = []
+
+    def one_step(record):
+        for _ in range(a.sweeps_per_step):
+            for _p in range(passes_per_sweep):
+                if record:
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    sim.run_pass()
+                    e1.record(stream)
+                    pass_events.append((e0, e1))
+                else:
+                    sim.run_pass()
+        return sim.observe(ccl=not a.no_ccl)
+
+    for _ in range(a.warmup):
+        one_step(False)
+    torch.cuda.synchronize()
+    launches0 = kk.launch_count()
+    hbm_peak, sm_max_mhz, peak_src = measured_peaks()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(a.steps):
+            obs = one_step(True)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    launches = kk.launch_count() - launches0
+    ms = t0.elapsed_time(t1)
+    pass_ms = [e0.elapsed_time(e1) for e0, e1 in pass_events]
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / a.steps
+    updates_per_step = a.sweeps_per_step * Lx * Ly  # all ranks
+    value = updates_per_step * a.steps / (ms / 1e3)
+
+    # ---- roofline of the dominant kernel (pass_kernel), from live event timings
+    pass_avg_s = float(np.mean(pass_ms)) / 1e3
+    upd_per_launch = N_local * a.T / 16
+    hbm_bytes_per_launch = 2 * N_local / 8  # read + write every site bit once (algorithmic)
+    hbm_achieved = hbm_bytes_per_launch / pass_avg_s / 1e9
+    cnt = kernel_counters()
+    alu_peak = 148 * 128 * sm_max_mhz * 1e6 / 1e12  # lane-ops/s: 148 SM x 128 INT/FP32 lanes x clock
+    if cnt and cnt.get("T") == a.T:
+        lane_ops = cnt["thread_inst_per_update"] * upd_per_launch
+        achieved = lane_ops / pass_avg_s / 1e12
+        traffic = cnt.get("dram_bytes_per_update")
+        traffic = traffic * upd_per_launch if traffic is not None else None
+        roof = {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "Tlane-op/s",
+                "frac": achieved / alu_peak, "traffic": traffic,
+                "peak_source": f"148 SMs x 128 lanes x {sm_max_mhz:.0f} MHz (max SM clock, {peak_src})",
+                "per_launch_ops": lane_ops, "ops_source": cnt.get("source")}
+    else:
+        roof = {"bound": "alu", "achieved": None, "peak": alu_peak, "unit": "Tlane-op/s",
+                "frac": None, "traffic": None, "note": "no ncu counters for this T yet"}
+    roof["kernel"] = "pass_kernel"
+    roof["launch_ms"] = pass_avg_s * 1e3
+    roof["share_of_step"] = float(np.sum(pass_ms)) / (ms / 1.0) if ms > 0 else None
+    roof["hbm"] = {"achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s",
+                   "frac": hbm_achieved / hbm_peak, "bytes_per_launch": hbm_bytes_per_launch,
+                   "peak_source": peak_src}
+
+    # ---- end to end through the public API: H2D of the step's lattice from pinned
+    # host memory, the step, D2H of the observables (and of the lattice)
+    e2e = None
+    if not a.no_e2e:
+        host = torch.empty(sim.packed_words(), dtype=torch.int32, pin_memory=True)
+        sim.download_packed(host.data_ptr())
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        w0 = time.perf_counter()
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(a.steps):
+            sim.upload_packed(host.data_ptr())
+            one_step(False)
+            sim.download_packed(host.data_ptr())
+        s1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - w0
+        e_ms = max(s0.elapsed_time(s1), wall * 1e3)
+        if dist:
+            t = torch.tensor([e_ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        nbytes = sim.packed_words() * 4
+        e2e = {"value": updates_per_step * a.steps / (e_ms / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": nbytes * world, "d2h_bytes_per_step": nbytes * world + 8 * 8,
+               "note": "per step: pinned-host->HBM lattice upload, S sweeps + observables, lattice download"}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u1", "data": "synthetic",
+            "config": {"workload": f"configs[4]: {Lx}x{rows} slab per GPU (global {Lx}x{Ly}), "
+                                   f"{a.sweeps_per_step} sweeps + observables"
+                                   + ("" if a.no_ccl else " + cluster histogram") + " per step",
+                       "omega_kT": a.omega, "fraction_A": a.fraction, "start": "random",
+                       "iters_per_pass": a.T, "parallelism": f"slab{world}",
+                       "l2": "inputs larger than L2 (2 x 512 MiB bit-packed per GPU)"},
+            "roofline": roof,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "e2e": e2e,
+            "observables": obs,
+        }
+        if world == 1 and not a.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(a.cpu_seconds, a.omega, a.fraction, a.seed)
+        print(json.dumps(out), flush=True)
+    sim.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

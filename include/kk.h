@@ -1,0 +1,190 @@
+/*
+ * kk.h — C ABI of the B200-native MPKK library (libkk.so).
+ *
+ * Massive Parallel Kawasaki Kinetics (MPKK) of arXiv:1309.4349 on a
+ * two-component triangular lipid lattice: Metropolis–Hastings Kawasaki
+ * exchange sweeps ("Massive Parallel Kawasaki Kinetics";
+ * PAPER.md:59-65 Metropolis listing), the one-parameter interaction
+ * omega_AB = g_AB - (g_AA + g_BB)/2 in units of kT, exact
+ * conservation of both species, and the cluster analysis of
+ * PAPER.md:138-140.  Readings R1..R11 referenced below are listed in
+ * DESIGN.md §8(c).
+ *
+ * Conventions for every entry point
+ *  - Lattice site (x, y), 0 <= x < Lx, 0 <= y < Ly; triangular lattice in axial
+ *    coordinates, periodic in x and y (R1, R2).  Value 1 = lipid A, 0 = lipid B.
+ *  - Device layout (owned by the handle): per replica, Ly rows of
+ *    W = ceil(Lx/32) uint32 words; site (x, y) is bit (x % 32) of word
+ *    y*W + x/32; bits >= Lx of a row's last word are always 0.
+ *  - "host" pointers are ordinary CPU memory (pinned or pageable); "device"
+ *    pointers are CUDA global memory on the handle's device.  The library never
+ *    takes ownership of caller memory.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *    stream).  Calls that write host outputs synchronise `stream` first.
+ *  - Return value: KK_OK (0) or a negative kk_status; the last error message of
+ *    the calling thread is available from kk_last_error().  No call aborts the
+ *    process; CUDA errors are reported as KK_ERR_CUDA.
+ *  - Requirements (R10): Lx % 8 == 0, Ly % 4 == 0, Lx >= 8, Ly >= 4.
+ */
+#ifndef KK_H_
+#define KK_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    KK_OK = 0,
+    KK_ERR_ARG = -1,        /* invalid argument (message says which) */
+    KK_ERR_CUDA = -2,       /* CUDA runtime error (message has cudaGetErrorString) */
+    KK_ERR_NOMEM = -3,      /* device or host allocation failed */
+    KK_ERR_CAPACITY = -4,   /* caller buffer too small; *n_out holds the size needed */
+    KK_ERR_STATE = -5       /* call not valid for this handle (e.g. kk_sweep on a slab) */
+} kk_status;
+
+typedef struct kk_lattice* kk_handle;
+
+/* Initial configuration (Fig. 6 "non-random configuration";
+ * PAPER.md:180 Fig. 10 "random and non-random start"), reading R7:
+ * n_A = floor(fraction_A * Lx * Ly_global + 0.5) sites are A. */
+typedef enum {
+    KK_INIT_RANDOM = 0,     /* the n_A sites with smallest Philox init keys (R6, R7) */
+    KK_INIT_BLOCK = 1,      /* the first n_A sites in row-major order */
+    KK_INIT_EMPTY = 2       /* all B; fill with kk_set_lattice* */
+} kk_init_mode;
+
+typedef struct {
+    int64_t Lx;             /* row length (sites), multiple of 8 */
+    int64_t Ly;             /* rows of the FULL lattice, multiple of 4 */
+    int64_t y_begin;        /* first global row held by this handle (slab), multiple of 4 */
+    int64_t y_count;        /* rows held (slab height), multiple of 4; = Ly for a full lattice */
+    int64_t replicas;       /* independent lattices (BASELINE configs[3]); >= 1, < 2^24 */
+    double fraction_A;      /* in [0, 1] */
+    double omega_kT;        /* omega_AB / kT, finite */
+    uint64_t seed;          /* Philox key (R6) */
+    int32_t init_mode;      /* kk_init_mode */
+    int32_t iters_per_pass; /* T in {1,2,4,8}: MPKK iterations fused per HBM pass; 0 = default (4) */
+    int32_t device;         /* CUDA device ordinal; -1 = current */
+    int32_t reserved;
+} kk_config;
+
+/* Create a full periodic Lx x Ly lattice (one replica) on the current device,
+ * initialised with KK_INIT_RANDOM.  Entry point named by north_star:
+ * kk_create(Lx, Ly, fraction_A, omega_kT, seed).  *out receives the handle. */
+int kk_create(kk_handle* out, int64_t Lx, int64_t Ly, double fraction_A,
+              double omega_kT, uint64_t seed);
+
+/* General constructor: replicas and/or a row slab [y_begin, y_begin+y_count)
+ * of a larger lattice (multi-GPU, north_star "slab-partitioned by rows").
+ * A slab handle needs halo rows from its neighbours for every pass
+ * (kk_pass); a handle with y_count == Ly is periodic by itself. */
+int kk_create_ex(kk_handle* out, const kk_config* cfg);
+
+int kk_destroy(kk_handle h);
+
+/* Run n MPKK sweeps (n Monte Carlo steps; R4): each sweep
+ * is 16 iterations; iteration j draws a centre class k_j (R6) and performs one
+ * Kawasaki exchange attempt per centre.  Sweep indices continue from the
+ * handle's sweep counter.  Only for full-lattice handles (KK_ERR_STATE on a
+ * slab).  Asynchronous on `stream`. */
+int kk_sweep(kk_handle h, int64_t n, void* stream);
+
+/* Energy per replica (R3): nab_out[r] = N_AB (unlike nearest-neighbour pairs,
+ * host, `replicas` entries); energy_out[r] = omega_kT * N_AB in kT (host, may
+ * be NULL).  For a slab, counts the bonds from each of its rows to the row
+ * above (x, y+1) and (x+1, y+1), using halo_bot (device, W words per replica,
+ * the first row of the next slab) for the last row — so the sum over slabs is
+ * the total. halo_bot is ignored (may be NULL) for full lattices. */
+int kk_energy(kk_handle h, int64_t* nab_out, double* energy_out,
+              const uint32_t* halo_bot, void* stream);
+
+/* Number of A sites per replica (host, `replicas` entries); conserved exactly
+ * by every sweep. */
+int kk_composition(kk_handle h, int64_t* na_out, void* stream);
+
+/* Counters accumulated by sweeps/passes since the last reset, per replica,
+ * over the centres this handle owns: attempted exchanges (N per sweep),
+ * trivial (same-type partner), accepted, and the summed N_AB change of
+ * accepted exchanges.  out: host array of 4*replicas int64 in that order. */
+int kk_stats(kk_handle h, int64_t* out, int reset, void* stream);
+
+/* Cluster-size histogram (Figs. 9-11; R9): clusters of
+ * `target` (1 = A, 0 = B) sites connected through the six neighbours on the
+ * periodic lattice.  Writes rows (replica, size, count) sorted by replica then
+ * size to out (host, 3*capacity int64); *n_out = rows written.  If capacity is
+ * too small returns KK_ERR_CAPACITY with *n_out = rows needed.  Full-lattice
+ * handles only. */
+int kk_cluster_histogram(kk_handle h, int target, int64_t* out, int64_t capacity,
+                         int64_t* n_out, void* stream);
+
+/* Lattice transfer.  Byte form: host uint8[replicas][y_count][Lx], 1 = A.
+ * Packed form: host uint32[replicas][y_count][W] in the device layout.  The
+ * packed form is what end-to-end callers use (1 bit per site). */
+int kk_get_lattice(kk_handle h, uint8_t* out, void* stream);
+int kk_set_lattice(kk_handle h, const uint8_t* in, void* stream);
+int kk_get_lattice_packed(kk_handle h, uint32_t* out, void* stream);
+int kk_set_lattice_packed(kk_handle h, const uint32_t* in, void* stream);
+/* Device-to-device variants (in/out are device pointers, same packed layout). */
+int kk_copy_lattice_packed_device(kk_handle h, uint32_t* dst, int to_device_buffer,
+                                  const uint32_t* src, void* stream);
+
+/* Random start for slab handles (R7), which need a selection over ALL slabs:
+ * create with KK_INIT_EMPTY, then
+ *   for level 0,1,2: kk_init_select_hist(level, prefix) -> hist (host,
+ *     replicas x 2048 int64: level 0 bins key[31:21], level 1 key[20:10] among
+ *     key[31:21] == prefix, level 2 key[9:0] among key[31:10] == prefix); sum
+ *     hist over slabs; pick per replica the bin where the cumulative count
+ *     reaches the remaining need; prefix = prefix<<11|bin (<<10 at level 2);
+ *   kk_init_select_ties(K = final prefix) -> (replica, global row-major index)
+ *     pairs of sites whose key == K (host, 2*capacity int64; KK_ERR_CAPACITY
+ *     and *n_out = needed if too small); gather over slabs, sort, cut = index
+ *     of the last tie taken + 1 (0 if none);
+ *   kk_init_select_apply(K, cut): site is A iff key < K or (key == K and
+ *     global index < cut).
+ * prefix, K: host uint32 per replica; cut: host int64 per replica.  Full
+ * lattices do all of this inside kk_create_ex. */
+int kk_init_select_hist(kk_handle h, int level, const uint32_t* prefix, int64_t* hist_out, void* stream);
+int kk_init_select_ties(kk_handle h, const uint32_t* K, int64_t* out, int64_t capacity, int64_t* n_out,
+                        void* stream);
+int kk_init_select_apply(kk_handle h, const uint32_t* K, const int64_t* cut, void* stream);
+
+/* Acceptance thresholds actually used (R5): out[v+3], v = dN_AB/2 in -3..3,
+ * accept iff u32 <= out[v+3] (and the pair is unlike). Host, 7 entries. */
+int kk_acceptance_table(kk_handle h, uint32_t* out);
+
+/* Geometry queries. */
+int kk_words_per_row(kk_handle h, int64_t* w);
+int kk_halo_rows(kk_handle h, int64_t* rows);     /* hy = 3T (R8) */
+int kk_sweep_index(kk_handle h, int64_t* s);      /* next sweep index */
+
+/* ---- slab passes (multi-GPU driver, north_star "per-phase halo-row exchange
+ * ... overlapped with interior updates").  One pass = T iterations of the
+ * current sweep.  Usage per pass:
+ *   kk_pack_halo(h, send_top, send_bot, s)     rows [0,hy) and [y_count-hy, y_count)
+ *   exchange send_top -> previous slab's halo_bot, send_bot -> next slab's halo_top
+ *   kk_pass(h, KK_REGION_INTERIOR, NULL, NULL, s2)   overlaps the exchange
+ *   kk_pass(h, KK_REGION_BOUNDARY, halo_top, halo_bot, s)
+ *   kk_pass_commit(h)                          flips buffers, advances (sweep, j)
+ * halo buffers: device, replicas * hy * W words, row-major like the lattice;
+ * halo_top holds global rows [y_begin-hy, y_begin), halo_bot rows
+ * [y_begin+y_count, +hy).  For a full-lattice handle halos may be NULL
+ * (rows wrap). */
+enum { KK_REGION_ALL = 0, KK_REGION_INTERIOR = 1, KK_REGION_BOUNDARY = 2 };
+int kk_pack_halo(kk_handle h, uint32_t* send_top, uint32_t* send_bot, void* stream);
+int kk_pass(kk_handle h, int region, const uint32_t* halo_top, const uint32_t* halo_bot,
+            void* stream);
+int kk_pass_commit(kk_handle h);
+
+/* Kernel launches issued by this thread's calls since process start (the
+ * bench's gpu_launches claim). */
+int64_t kk_launch_count(void);
+
+const char* kk_last_error(void);
+const char* kk_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KK_H_ */

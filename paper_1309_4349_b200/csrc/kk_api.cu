@@ -1,0 +1,694 @@
+// kk_api.cu — the C ABI (include/kk.h): handle lifecycle, host orchestration
+// of the kernels, argument checking and error reporting.  Host-side logic
+// only: every step of the simulation itself runs in the kernels of
+// kk_pass.cu / kk_observe.cu / kk_ccl.cu.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/kk.h"
+#include "kk_internal.cuh"
+
+namespace kk {
+
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+int pass_smem_bytes(int T, int THI, int TWI);
+cudaError_t launch_pass(int T, const PassParams& P, int grid_y, int replicas, cudaStream_t stream);
+cudaError_t launch_observe(const ObsParams& P, cudaStream_t s);
+cudaError_t launch_init_block(uint32_t* lat, const Geom& g, int64_t replicas, int64_t nA, cudaStream_t s);
+cudaError_t launch_select_hist(const Geom& g, int64_t rep0, int64_t nrep, int level, const uint32_t* prefix,
+                               unsigned long long* hist, uint32_t k0, uint32_t k1, cudaStream_t s);
+cudaError_t launch_select_ties(const Geom& g, int64_t rep0, int64_t nrep, const uint32_t* K, long long* out,
+                               unsigned long long* count, int64_t cap, uint32_t k0, uint32_t k1, cudaStream_t s);
+cudaError_t launch_select_apply(uint32_t* lat, const Geom& g, int64_t rep0, int64_t nrep, const uint32_t* K,
+                                const long long* cut, uint32_t k0, uint32_t k1, cudaStream_t s);
+cudaError_t launch_pack(const uint8_t* bytes, uint32_t* lat, const Geom& g, int64_t replicas, cudaStream_t s);
+cudaError_t launch_unpack(const uint32_t* lat, uint8_t* bytes, const Geom& g, int64_t replicas, cudaStream_t s);
+cudaError_t launch_pack_halo(const uint32_t* lat, uint32_t* top, uint32_t* bot, const Geom& g, int64_t replicas,
+                             int hy, cudaStream_t s);
+template <typename L>
+cudaError_t launch_ccl(const uint32_t* lat, const Geom& g, int64_t replicas, int target, L* lab, L* cnt,
+                       unsigned int* hist, unsigned long long* big, unsigned long long* nbig, int64_t big_cap,
+                       cudaStream_t s);
+
+}  // namespace kk
+
+using namespace kk;
+
+struct kk_lattice {
+    int device = 0;
+    Geom g{};
+    int64_t R = 1;
+    double fraction_A = 0.5, omega = 0.0;
+    uint64_t seed = 0;
+    int T = 4, hy = 12;
+    uint32_t* buf[2] = {nullptr, nullptr};
+    int cur = 0;
+    unsigned long long* stats = nullptr;  // device [R][4]
+    unsigned long long* obs = nullptr;    // device [R][2]
+    uint32_t thr[7] = {0};
+    int64_t sweep = 0;
+    int j = 0;
+    int THI = 0, TWI = 0, tiles_x = 0, bands = 0, b_lo = 0, b_hi = 0;
+    // cluster analysis (lazy)
+    void* lab = nullptr;
+    void* cnt = nullptr;
+    int lab64 = 0;
+    unsigned int* hist = nullptr;
+    unsigned long long* big = nullptr;
+    unsigned long long* nbig = nullptr;
+    int64_t big_cap = 0;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define KK_CUDA(expr)                                                                       \
+    do {                                                                                    \
+        cudaError_t _e = (expr);                                                            \
+        if (_e != cudaSuccess)                                                              \
+            return fail(KK_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));  \
+    } while (0)
+
+#define KK_CHECK_HANDLE(h)                                                   \
+    do {                                                                     \
+        if (!(h)) return fail(KK_ERR_ARG, "null handle");                    \
+        if ((h)->device >= 0) {                                              \
+            cudaError_t _e = cudaSetDevice((h)->device);                     \
+            if (_e != cudaSuccess)                                           \
+                return fail(KK_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(_e)); \
+        }                                                                    \
+    } while (0)
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return (v && *v) ? std::atoi(v) : dflt;
+}
+
+int64_t count_a_for(int64_t N, double f) { return (int64_t)std::floor(f * (double)N + 0.5); }
+
+// R5: accept iff u32 <= thr[v+3], thr = ceil(exp(-dE) 2^32) - 1, dE = omega*2v.
+void make_thresholds(double omega, uint32_t thr[7]) {
+    for (int v = -3; v <= 3; ++v) {
+        const double dE = omega * (double)(2 * v);
+        if (dE <= 0.0) {
+            thr[v + 3] = 0xFFFFFFFFu;
+        } else {
+            const double t = std::ceil(std::exp(-dE) * 4294967296.0);
+            thr[v + 3] = (uint32_t)(t - 1.0);
+        }
+    }
+}
+
+void choose_tiles(kk_lattice* h) {
+    const int twi_t = std::max(1, env_int("KK_TWI", 64));
+    const int thi_t = std::max(4, env_int("KK_THI", 256));
+    const int64_t W = h->g.W, rows = h->g.rows;
+    const int64_t nx = (W + twi_t - 1) / twi_t;
+    h->TWI = (int)((W + nx - 1) / nx);
+    h->tiles_x = (int)((W + h->TWI - 1) / h->TWI);
+    const int64_t nb = (rows + thi_t - 1) / thi_t;
+    int64_t thi = (rows + nb - 1) / nb;
+    thi = (thi + 3) / 4 * 4;
+    h->THI = (int)thi;
+    h->bands = (int)((rows + thi - 1) / thi);
+    // slab mode: bands whose loaded rows [b*THI - hy, (b+1)*THI + hy) are local
+    h->b_lo = (int)((h->hy + thi - 1) / thi);
+    h->b_hi = (int)std::max<int64_t>(0, (rows - h->hy) / thi);
+    if (h->b_hi < h->b_lo) h->b_hi = h->b_lo;
+    if (h->b_hi > h->bands) h->b_hi = h->bands;
+    if (h->b_lo > h->bands) h->b_lo = h->b_hi = h->bands;
+}
+
+PassParams make_pass_params(kk_lattice* h, const uint32_t* ht, const uint32_t* hb) {
+    PassParams P{};
+    P.src = h->buf[h->cur];
+    P.dst = h->buf[h->cur ^ 1];
+    P.halo_top = ht;
+    P.halo_bot = hb;
+    P.stats = h->stats;
+    P.g = h->g;
+    P.halo_rep_words = (int64_t)h->hy * h->g.W;
+    P.THI = h->THI;
+    P.TWI = h->TWI;
+    P.tiles_x = h->tiles_x;
+    P.sweep = (uint32_t)h->sweep;
+    P.j0 = h->j;
+    P.key0 = (uint32_t)(h->seed & 0xFFFFFFFFu);
+    P.key1 = (uint32_t)(h->seed >> 32);
+    for (int k = 0; k < 7; ++k) P.thr[k] = h->thr[k];
+    return P;
+}
+
+int run_pass(kk_lattice* h, int region, const uint32_t* ht, const uint32_t* hb, cudaStream_t s) {
+    PassParams P = make_pass_params(h, ht, hb);
+    int grid_y = 0;
+    if (region == KK_REGION_ALL) {
+        P.nA = h->bands; P.bA = 0; P.bB = 0;
+        grid_y = h->bands;
+    } else if (region == KK_REGION_INTERIOR) {
+        P.nA = h->b_hi - h->b_lo; P.bA = h->b_lo; P.bB = 0;
+        grid_y = P.nA;
+    } else if (region == KK_REGION_BOUNDARY) {
+        P.nA = h->b_lo; P.bA = 0; P.bB = h->b_hi;
+        grid_y = h->b_lo + (h->bands - h->b_hi);
+    } else {
+        return fail(KK_ERR_ARG, "kk_pass: bad region");
+    }
+    KK_CUDA(launch_pass(h->T, P, grid_y, (int)h->R, s));  // grid.z = replica (R <= 65535)
+    return KK_OK;
+}
+
+void free_all(kk_lattice* h) {
+    cudaFree(h->buf[0]);
+    cudaFree(h->buf[1]);
+    cudaFree(h->stats);
+    cudaFree(h->obs);
+    cudaFree(h->lab);
+    cudaFree(h->cnt);
+    cudaFree(h->hist);
+    cudaFree(h->big);
+    cudaFree(h->nbig);
+}
+
+// ---- exact-composition random start (R7): radix select in three steps.
+// Each step works on this handle's rows; for a slab the caller sums the
+// histograms / gathers the ties over all slabs between steps.
+int select_hist(kk_lattice* h, int level, const uint32_t* prefix, int64_t* hist_out, cudaStream_t s) {
+    const uint32_t k0 = (uint32_t)(h->seed & 0xFFFFFFFFu), k1 = (uint32_t)(h->seed >> 32);
+    for (int64_t r0 = 0; r0 < h->R; r0 += 65535) {
+        const int64_t nr = std::min<int64_t>(65535, h->R - r0);
+        unsigned long long* dhist = nullptr;
+        uint32_t* dpre = nullptr;
+        KK_CUDA(cudaMalloc(&dhist, sizeof(unsigned long long) * nr * 2048));
+        KK_CUDA(cudaMalloc(&dpre, sizeof(uint32_t) * nr));
+        KK_CUDA(cudaMemsetAsync(dhist, 0, sizeof(unsigned long long) * nr * 2048, s));
+        if (prefix) KK_CUDA(cudaMemcpyAsync(dpre, prefix + r0, sizeof(uint32_t) * nr, cudaMemcpyHostToDevice, s));
+        else KK_CUDA(cudaMemsetAsync(dpre, 0, sizeof(uint32_t) * nr, s));
+        KK_CUDA(launch_select_hist(h->g, r0, nr, level, dpre, dhist, k0, k1, s));
+        KK_CUDA(cudaMemcpyAsync(hist_out + r0 * 2048, dhist, sizeof(unsigned long long) * nr * 2048,
+                                cudaMemcpyDeviceToHost, s));
+        KK_CUDA(cudaStreamSynchronize(s));
+        cudaFree(dhist);
+        cudaFree(dpre);
+    }
+    return KK_OK;
+}
+
+int select_ties(kk_lattice* h, const uint32_t* K, int64_t* out, int64_t capacity, int64_t* n_out, cudaStream_t s) {
+    const uint32_t k0 = (uint32_t)(h->seed & 0xFFFFFFFFu), k1 = (uint32_t)(h->seed >> 32);
+    int64_t total = 0;
+    for (int64_t r0 = 0; r0 < h->R; r0 += 65535) {
+        const int64_t nr = std::min<int64_t>(65535, h->R - r0);
+        const int64_t cap = std::max<int64_t>(0, capacity - total);
+        uint32_t* dK = nullptr;
+        long long* dties = nullptr;
+        unsigned long long* dcount = nullptr;
+        KK_CUDA(cudaMalloc(&dK, sizeof(uint32_t) * nr));
+        KK_CUDA(cudaMalloc(&dties, sizeof(long long) * 2 * std::max<int64_t>(cap, 1)));
+        KK_CUDA(cudaMalloc(&dcount, sizeof(unsigned long long)));
+        KK_CUDA(cudaMemsetAsync(dcount, 0, sizeof(unsigned long long), s));
+        KK_CUDA(cudaMemcpyAsync(dK, K + r0, sizeof(uint32_t) * nr, cudaMemcpyHostToDevice, s));
+        KK_CUDA(launch_select_ties(h->g, r0, nr, dK, dties, dcount, cap, k0, k1, s));
+        unsigned long long nt = 0;
+        KK_CUDA(cudaMemcpyAsync(&nt, dcount, sizeof(nt), cudaMemcpyDeviceToHost, s));
+        KK_CUDA(cudaStreamSynchronize(s));
+        const int64_t got = std::min<int64_t>((int64_t)nt, cap);
+        if (got > 0 && out) {
+            std::vector<long long> tmp(2 * got);
+            KK_CUDA(cudaMemcpyAsync(tmp.data(), dties, sizeof(long long) * 2 * got, cudaMemcpyDeviceToHost, s));
+            KK_CUDA(cudaStreamSynchronize(s));
+            for (int64_t t = 0; t < got; ++t) {
+                out[2 * (total + t)] = tmp[2 * t] + r0;
+                out[2 * (total + t) + 1] = tmp[2 * t + 1];
+            }
+        }
+        total += (int64_t)nt;
+        cudaFree(dK);
+        cudaFree(dties);
+        cudaFree(dcount);
+    }
+    *n_out = total;
+    if (total > capacity) return fail(KK_ERR_CAPACITY, "tie buffer too small");
+    return KK_OK;
+}
+
+int select_apply(kk_lattice* h, const uint32_t* K, const int64_t* cut, cudaStream_t s) {
+    const uint32_t k0 = (uint32_t)(h->seed & 0xFFFFFFFFu), k1 = (uint32_t)(h->seed >> 32);
+    for (int64_t r0 = 0; r0 < h->R; r0 += 65535) {
+        const int64_t nr = std::min<int64_t>(65535, h->R - r0);
+        uint32_t* dK = nullptr;
+        long long* dcut = nullptr;
+        KK_CUDA(cudaMalloc(&dK, sizeof(uint32_t) * nr));
+        KK_CUDA(cudaMalloc(&dcut, sizeof(long long) * nr));
+        KK_CUDA(cudaMemcpyAsync(dK, K + r0, sizeof(uint32_t) * nr, cudaMemcpyHostToDevice, s));
+        KK_CUDA(cudaMemcpyAsync(dcut, cut + r0, sizeof(long long) * nr, cudaMemcpyHostToDevice, s));
+        KK_CUDA(launch_select_apply(h->buf[h->cur], h->g, r0, nr, dK, dcut, k0, k1, s));
+        KK_CUDA(cudaStreamSynchronize(s));
+        cudaFree(dK);
+        cudaFree(dcut);
+    }
+    return KK_OK;
+}
+
+// Bin choice of one radix-select level (host): the smallest bin b whose
+// cumulative count reaches need[r]; need[r] becomes the rank inside bin b.
+void select_choose(int level, const int64_t* hist, int64_t R, int64_t* need, uint32_t* prefix) {
+    const int nbins = level == 2 ? 1024 : 2048;
+    for (int64_t r = 0; r < R; ++r) {
+        int64_t cum = 0;
+        int b = 0;
+        for (; b < nbins; ++b) {
+            const int64_t c = hist[r * 2048 + b];
+            if (cum + c >= need[r]) break;
+            cum += c;
+        }
+        if (b == nbins) b = nbins - 1;
+        need[r] -= cum;
+        prefix[r] = (prefix[r] << (level == 2 ? 10 : 11)) | (uint32_t)b;
+    }
+}
+
+int init_random_full(kk_lattice* h, cudaStream_t s) {
+    const int64_t R = h->R;
+    const int64_t nA = count_a_for(h->g.Lx * h->g.Ly, h->fraction_A);
+    std::vector<int64_t> need(R, nA), hist(R * 2048);
+    std::vector<uint32_t> prefix(R, 0);
+    for (int level = 0; level < 3; ++level) {
+        int rc = select_hist(h, level, level ? prefix.data() : nullptr, hist.data(), s);
+        if (rc != KK_OK) return rc;
+        select_choose(level, hist.data(), R, need.data(), prefix.data());
+    }
+    // prefix now holds the 32-bit cut key K; need = number of ties to take
+    int64_t ntie = 0;
+    for (int64_t r = 0; r < R; ++r) ntie += hist[r * 2048 + (prefix[r] & 1023u)];
+    std::vector<int64_t> ties(2 * std::max<int64_t>(ntie, 1));
+    int64_t n_out = 0;
+    int rc = select_ties(h, prefix.data(), ties.data(), ntie, &n_out, s);
+    if (rc != KK_OK) return rc;
+    std::vector<std::vector<int64_t>> per(R);
+    for (int64_t t = 0; t < n_out; ++t) per[ties[2 * t]].push_back(ties[2 * t + 1]);
+    std::vector<int64_t> cut(R, 0);
+    for (int64_t r = 0; r < R; ++r) {
+        std::sort(per[r].begin(), per[r].end());
+        if (need[r] > (int64_t)per[r].size()) return fail(KK_ERR_STATE, "init: tie count mismatch");
+        cut[r] = need[r] > 0 ? per[r][need[r] - 1] + 1 : 0;
+    }
+    return select_apply(h, prefix.data(), cut.data(), s);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* kk_last_error(void) { return g_err.c_str(); }
+const char* kk_version(void) { return "kk 0.1 (sm_100a, MPKK 4x4 centre classes, Philox4x32-10)"; }
+int64_t kk_launch_count(void) { return (int64_t)g_launches.load(); }
+
+int kk_create_ex(kk_handle* out, const kk_config* c) {
+    if (!out || !c) return fail(KK_ERR_ARG, "null argument");
+    *out = nullptr;
+    if (c->Lx < 8 || c->Lx % 8) return fail(KK_ERR_ARG, "Lx must be a positive multiple of 8 (DESIGN.md R10)");
+    if (c->Ly < 4 || c->Ly % 4) return fail(KK_ERR_ARG, "Ly must be a positive multiple of 4 (DESIGN.md R10)");
+    if (c->y_count < 4 || c->y_count % 4 || c->y_begin < 0 || c->y_begin % 4 || c->y_begin + c->y_count > c->Ly)
+        return fail(KK_ERR_ARG, "slab [y_begin, y_begin+y_count) must be inside [0, Ly) in multiples of 4");
+    if (c->replicas < 1 || c->replicas >= (1 << 16)) return fail(KK_ERR_ARG, "replicas must be in [1, 65535]");
+    if (!(c->fraction_A >= 0.0 && c->fraction_A <= 1.0)) return fail(KK_ERR_ARG, "fraction_A must be in [0,1]");
+    if (!std::isfinite(c->omega_kT)) return fail(KK_ERR_ARG, "omega_kT must be finite");
+    const int T = c->iters_per_pass ? c->iters_per_pass : env_int("KK_T", 4);
+    if (T != 1 && T != 2 && T != 4 && T != 8) return fail(KK_ERR_ARG, "iters_per_pass must be 1, 2, 4 or 8");
+    if (c->init_mode < 0 || c->init_mode > 2) return fail(KK_ERR_ARG, "bad init_mode");
+    const bool slab = c->y_count != c->Ly;
+    if (slab && c->y_count < 3 * T) return fail(KK_ERR_ARG, "slab must hold at least 3*T rows (halo depth)");
+    if (slab && c->init_mode == KK_INIT_RANDOM)
+        return fail(KK_ERR_ARG, "slab handles: random start needs the distributed selection (use KK_INIT_EMPTY)");
+
+    kk_lattice* h = new kk_lattice();
+    h->device = c->device;
+    if (h->device >= 0) {
+        cudaError_t e = cudaSetDevice(h->device);
+        if (e != cudaSuccess) { delete h; return fail(KK_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e)); }
+    } else {
+        cudaGetDevice(&h->device);
+    }
+    h->g.Lx = c->Lx;
+    h->g.W = (int32_t)((c->Lx + 31) / 32);
+    h->g.tail = (int32_t)(c->Lx % 32);
+    h->g.rows = c->y_count;
+    h->g.y_begin = c->y_begin;
+    h->g.Ly = c->Ly;
+    h->g.rep_words = c->y_count * h->g.W;
+    h->g.periodic = slab ? 0 : 1;
+    h->R = c->replicas;
+    h->fraction_A = c->fraction_A;
+    h->omega = c->omega_kT;
+    h->seed = c->seed;
+    h->T = T;
+    h->hy = 3 * T;
+    make_thresholds(h->omega, h->thr);
+    choose_tiles(h);
+    if (pass_smem_bytes(T, h->THI, h->TWI) > 227 * 1024) {
+        delete h;
+        return fail(KK_ERR_ARG, "tile too large for shared memory (KK_THI/KK_TWI)");
+    }
+    const size_t words = (size_t)h->R * (size_t)h->g.rep_words;
+    cudaError_t e1 = cudaMalloc(&h->buf[0], words * 4);
+    cudaError_t e2 = cudaMalloc(&h->buf[1], words * 4);
+    cudaError_t e3 = cudaMalloc(&h->stats, sizeof(unsigned long long) * 4 * h->R);
+    cudaError_t e4 = cudaMalloc(&h->obs, sizeof(unsigned long long) * 2 * h->R);
+    if (e1 || e2 || e3 || e4) {
+        free_all(h);
+        delete h;
+        return fail(KK_ERR_NOMEM, "device allocation failed");
+    }
+    cudaStream_t s = nullptr;
+    int rc = KK_OK;
+    if (cudaMemsetAsync(h->buf[0], 0, words * 4, s) || cudaMemsetAsync(h->buf[1], 0, words * 4, s) ||
+        cudaMemsetAsync(h->stats, 0, sizeof(unsigned long long) * 4 * h->R, s)) {
+        rc = fail(KK_ERR_CUDA, "memset failed");
+    }
+    if (rc == KK_OK && c->init_mode == KK_INIT_BLOCK) {
+        cudaError_t e = launch_init_block(h->buf[0], h->g, h->R, count_a_for(c->Lx * c->Ly, c->fraction_A), s);
+        if (e != cudaSuccess) rc = fail(KK_ERR_CUDA, cudaGetErrorString(e));
+    } else if (rc == KK_OK && c->init_mode == KK_INIT_RANDOM) {
+        rc = init_random_full(h, s);
+    }
+    if (rc == KK_OK) {
+        cudaError_t e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) rc = fail(KK_ERR_CUDA, cudaGetErrorString(e));
+    }
+    if (rc != KK_OK) {
+        free_all(h);
+        delete h;
+        return rc;
+    }
+    *out = h;
+    return KK_OK;
+}
+
+int kk_create(kk_handle* out, int64_t Lx, int64_t Ly, double fraction_A, double omega_kT, uint64_t seed) {
+    kk_config c{};
+    c.Lx = Lx;
+    c.Ly = Ly;
+    c.y_begin = 0;
+    c.y_count = Ly;
+    c.replicas = 1;
+    c.fraction_A = fraction_A;
+    c.omega_kT = omega_kT;
+    c.seed = seed;
+    c.init_mode = KK_INIT_RANDOM;
+    c.iters_per_pass = 0;
+    c.device = -1;
+    return kk_create_ex(out, &c);
+}
+
+int kk_destroy(kk_handle h) {
+    if (!h) return KK_OK;
+    if (h->device >= 0) cudaSetDevice(h->device);
+    cudaDeviceSynchronize();
+    free_all(h);
+    delete h;
+    return KK_OK;
+}
+
+int kk_pass(kk_handle h, int region, const uint32_t* halo_top, const uint32_t* halo_bot, void* stream) {
+    KK_CHECK_HANDLE(h);
+    if (!h->g.periodic && (!halo_top || !halo_bot) && region != KK_REGION_INTERIOR)
+        return fail(KK_ERR_ARG, "slab pass needs both halo buffers");
+    return run_pass(h, region, halo_top, halo_bot, S(stream));
+}
+
+int kk_pass_commit(kk_handle h) {
+    if (!h) return fail(KK_ERR_ARG, "null handle");
+    h->cur ^= 1;
+    h->j += h->T;
+    if (h->j == 16) {
+        h->j = 0;
+        h->sweep += 1;
+    }
+    return KK_OK;
+}
+
+int kk_sweep(kk_handle h, int64_t n, void* stream) {
+    KK_CHECK_HANDLE(h);
+    if (!h->g.periodic) return fail(KK_ERR_STATE, "kk_sweep: slab handle (use kk_pass)");
+    if (n < 0) return fail(KK_ERR_ARG, "n must be >= 0");
+    const int64_t passes = n * (16 / h->T);
+    for (int64_t p = 0; p < passes; ++p) {
+        int rc = run_pass(h, KK_REGION_ALL, nullptr, nullptr, S(stream));
+        if (rc != KK_OK) return rc;
+        kk_pass_commit(h);
+    }
+    return KK_OK;
+}
+
+int kk_pack_halo(kk_handle h, uint32_t* send_top, uint32_t* send_bot, void* stream) {
+    KK_CHECK_HANDLE(h);
+    KK_CUDA(launch_pack_halo(h->buf[h->cur], send_top, send_bot, h->g, h->R, h->hy, S(stream)));
+    return KK_OK;
+}
+
+int kk_energy(kk_handle h, int64_t* nab_out, double* energy_out, const uint32_t* halo_bot, void* stream) {
+    KK_CHECK_HANDLE(h);
+    if (!nab_out) return fail(KK_ERR_ARG, "nab_out is null");
+    cudaStream_t s = S(stream);
+    KK_CUDA(cudaMemsetAsync(h->obs, 0, sizeof(unsigned long long) * 2 * h->R, s));
+    ObsParams P{};
+    P.lat = h->buf[h->cur];
+    P.halo_bot = h->g.periodic ? nullptr : halo_bot;
+    P.halo_stride = (int64_t)h->hy * h->g.W;
+    P.out = h->obs;
+    P.g = h->g;
+    P.replicas = h->R;
+    KK_CUDA(launch_observe(P, s));
+    std::vector<unsigned long long> v(2 * h->R);
+    KK_CUDA(cudaMemcpyAsync(v.data(), h->obs, sizeof(unsigned long long) * 2 * h->R, cudaMemcpyDeviceToHost, s));
+    KK_CUDA(cudaStreamSynchronize(s));
+    for (int64_t r = 0; r < h->R; ++r) {
+        nab_out[r] = (int64_t)v[2 * r];
+        if (energy_out) energy_out[r] = h->omega * (double)v[2 * r];
+    }
+    return KK_OK;
+}
+
+int kk_composition(kk_handle h, int64_t* na_out, void* stream) {
+    KK_CHECK_HANDLE(h);
+    if (!na_out) return fail(KK_ERR_ARG, "na_out is null");
+    cudaStream_t s = S(stream);
+    KK_CUDA(cudaMemsetAsync(h->obs, 0, sizeof(unsigned long long) * 2 * h->R, s));
+    ObsParams P{};
+    P.lat = h->buf[h->cur];
+    P.halo_bot = nullptr;
+    P.halo_stride = 0;
+    P.out = h->obs;
+    P.g = h->g;
+    P.replicas = h->R;
+    KK_CUDA(launch_observe(P, s));
+    std::vector<unsigned long long> v(2 * h->R);
+    KK_CUDA(cudaMemcpyAsync(v.data(), h->obs, sizeof(unsigned long long) * 2 * h->R, cudaMemcpyDeviceToHost, s));
+    KK_CUDA(cudaStreamSynchronize(s));
+    for (int64_t r = 0; r < h->R; ++r) na_out[r] = (int64_t)v[2 * r + 1];
+    return KK_OK;
+}
+
+int kk_stats(kk_handle h, int64_t* out, int reset, void* stream) {
+    KK_CHECK_HANDLE(h);
+    if (!out) return fail(KK_ERR_ARG, "out is null");
+    cudaStream_t s = S(stream);
+    KK_CUDA(cudaMemcpyAsync(out, h->stats, sizeof(int64_t) * 4 * h->R, cudaMemcpyDeviceToHost, s));
+    if (reset) KK_CUDA(cudaMemsetAsync(h->stats, 0, sizeof(unsigned long long) * 4 * h->R, s));
+    KK_CUDA(cudaStreamSynchronize(s));
+    return KK_OK;
+}
+
+int kk_cluster_histogram(kk_handle h, int target, int64_t* out, int64_t capacity, int64_t* n_out, void* stream) {
+    KK_CHECK_HANDLE(h);
+    if (!n_out) return fail(KK_ERR_ARG, "n_out is null");
+    if (!h->g.periodic) return fail(KK_ERR_STATE, "cluster histogram needs a full-lattice handle");
+    cudaStream_t s = S(stream);
+    const int64_t N = h->g.Lx * h->g.rows;
+    const int64_t n = N * h->R;
+    const bool need64 = N >= (int64_t)0xFFFFFFFFll;
+    if (!h->lab || (need64 != (bool)h->lab64)) {
+        cudaFree(h->lab);
+        cudaFree(h->cnt);
+        cudaFree(h->hist);
+        cudaFree(h->big);
+        cudaFree(h->nbig);
+        h->lab = h->cnt = nullptr;
+        h->hist = nullptr;
+        h->big = h->nbig = nullptr;
+        const size_t ls = need64 ? 8 : 4;
+        h->lab64 = need64;
+        h->big_cap = n / kDense + 16;
+        if (cudaMalloc(&h->lab, ls * n) || cudaMalloc(&h->cnt, ls * n) ||
+            cudaMalloc(&h->hist, sizeof(unsigned int) * kDense * h->R) ||
+            cudaMalloc(&h->big, sizeof(unsigned long long) * 2 * h->big_cap) ||
+            cudaMalloc(&h->nbig, sizeof(unsigned long long))) {
+            cudaGetLastError();
+            return fail(KK_ERR_NOMEM, "cluster buffers: device allocation failed");
+        }
+    }
+    KK_CUDA(cudaMemsetAsync(h->hist, 0, sizeof(unsigned int) * kDense * h->R, s));
+    KK_CUDA(cudaMemsetAsync(h->nbig, 0, sizeof(unsigned long long), s));
+    if (h->lab64) {
+        KK_CUDA(launch_ccl<unsigned long long>(h->buf[h->cur], h->g, h->R, target, (unsigned long long*)h->lab,
+                                               (unsigned long long*)h->cnt, h->hist, h->big, h->nbig, h->big_cap, s));
+    } else {
+        KK_CUDA(launch_ccl<uint32_t>(h->buf[h->cur], h->g, h->R, target, (uint32_t*)h->lab, (uint32_t*)h->cnt,
+                                     h->hist, h->big, h->nbig, h->big_cap, s));
+    }
+    std::vector<unsigned int> hist((size_t)kDense * h->R);
+    unsigned long long nb = 0;
+    KK_CUDA(cudaMemcpyAsync(hist.data(), h->hist, sizeof(unsigned int) * kDense * h->R, cudaMemcpyDeviceToHost, s));
+    KK_CUDA(cudaMemcpyAsync(&nb, h->nbig, sizeof(nb), cudaMemcpyDeviceToHost, s));
+    KK_CUDA(cudaStreamSynchronize(s));
+    if ((int64_t)nb > h->big_cap) return fail(KK_ERR_STATE, "cluster list overflow");
+    std::vector<unsigned long long> big(2 * nb);
+    if (nb) {
+        KK_CUDA(cudaMemcpyAsync(big.data(), h->big, sizeof(unsigned long long) * 2 * nb, cudaMemcpyDeviceToHost, s));
+        KK_CUDA(cudaStreamSynchronize(s));
+    }
+    std::vector<std::pair<int64_t, int64_t>> bigl(nb);
+    for (unsigned long long k = 0; k < nb; ++k) bigl[k] = {(int64_t)big[2 * k], (int64_t)big[2 * k + 1]};
+    std::sort(bigl.begin(), bigl.end());
+    std::vector<int64_t> rows;
+    size_t bi = 0;
+    for (int64_t r = 0; r < h->R; ++r) {
+        for (int sz = 1; sz < kDense; ++sz) {
+            const unsigned int c = hist[(size_t)r * kDense + sz];
+            if (c) { rows.push_back(r); rows.push_back(sz); rows.push_back(c); }
+        }
+        while (bi < bigl.size() && bigl[bi].first == r) {
+            const int64_t sz = bigl[bi].second;
+            int64_t c = 0;
+            while (bi < bigl.size() && bigl[bi].first == r && bigl[bi].second == sz) { ++c; ++bi; }
+            rows.push_back(r); rows.push_back(sz); rows.push_back(c);
+        }
+    }
+    const int64_t nrows = (int64_t)rows.size() / 3;
+    *n_out = nrows;
+    if (nrows > capacity || (!out && nrows > 0)) return fail(KK_ERR_CAPACITY, "histogram buffer too small");
+    if (nrows) std::memcpy(out, rows.data(), sizeof(int64_t) * rows.size());
+    return KK_OK;
+}
+
+int kk_get_lattice(kk_handle h, uint8_t* out, void* stream) {
+    KK_CHECK_HANDLE(h);
+    if (!out) return fail(KK_ERR_ARG, "out is null");
+    cudaStream_t s = S(stream);
+    const size_t n = (size_t)h->R * h->g.rows * h->g.Lx;
+    uint8_t* tmp = nullptr;
+    KK_CUDA(cudaMalloc(&tmp, n));
+    KK_CUDA(launch_unpack(h->buf[h->cur], tmp, h->g, h->R, s));
+    KK_CUDA(cudaMemcpyAsync(out, tmp, n, cudaMemcpyDeviceToHost, s));
+    KK_CUDA(cudaStreamSynchronize(s));
+    cudaFree(tmp);
+    return KK_OK;
+}
+
+int kk_set_lattice(kk_handle h, const uint8_t* in, void* stream) {
+    KK_CHECK_HANDLE(h);
+    if (!in) return fail(KK_ERR_ARG, "in is null");
+    cudaStream_t s = S(stream);
+    const size_t n = (size_t)h->R * h->g.rows * h->g.Lx;
+    uint8_t* tmp = nullptr;
+    KK_CUDA(cudaMalloc(&tmp, n));
+    KK_CUDA(cudaMemcpyAsync(tmp, in, n, cudaMemcpyHostToDevice, s));
+    KK_CUDA(launch_pack(tmp, h->buf[h->cur], h->g, h->R, s));
+    KK_CUDA(cudaStreamSynchronize(s));
+    cudaFree(tmp);
+    return KK_OK;
+}
+
+int kk_get_lattice_packed(kk_handle h, uint32_t* out, void* stream) {
+    KK_CHECK_HANDLE(h);
+    if (!out) return fail(KK_ERR_ARG, "out is null");
+    const size_t bytes = (size_t)h->R * h->g.rep_words * 4;
+    KK_CUDA(cudaMemcpyAsync(out, h->buf[h->cur], bytes, cudaMemcpyDeviceToHost, S(stream)));
+    KK_CUDA(cudaStreamSynchronize(S(stream)));
+    return KK_OK;
+}
+
+int kk_set_lattice_packed(kk_handle h, const uint32_t* in, void* stream) {
+    KK_CHECK_HANDLE(h);
+    if (!in) return fail(KK_ERR_ARG, "in is null");
+    const size_t bytes = (size_t)h->R * h->g.rep_words * 4;
+    KK_CUDA(cudaMemcpyAsync(h->buf[h->cur], in, bytes, cudaMemcpyHostToDevice, S(stream)));
+    KK_CUDA(cudaStreamSynchronize(S(stream)));
+    return KK_OK;
+}
+
+int kk_copy_lattice_packed_device(kk_handle h, uint32_t* dst, int to_device_buffer, const uint32_t* src,
+                                  void* stream) {
+    KK_CHECK_HANDLE(h);
+    const size_t bytes = (size_t)h->R * h->g.rep_words * 4;
+    if (to_device_buffer) {
+        if (!src) return fail(KK_ERR_ARG, "src is null");
+        KK_CUDA(cudaMemcpyAsync(h->buf[h->cur], src, bytes, cudaMemcpyDeviceToDevice, S(stream)));
+    } else {
+        if (!dst) return fail(KK_ERR_ARG, "dst is null");
+        KK_CUDA(cudaMemcpyAsync(dst, h->buf[h->cur], bytes, cudaMemcpyDeviceToDevice, S(stream)));
+    }
+    return KK_OK;
+}
+
+int kk_init_select_hist(kk_handle h, int level, const uint32_t* prefix, int64_t* hist_out, void* stream) {
+    KK_CHECK_HANDLE(h);
+    if (level < 0 || level > 2 || !hist_out || (level > 0 && !prefix)) return fail(KK_ERR_ARG, "bad select level/args");
+    return select_hist(h, level, prefix, hist_out, S(stream));
+}
+
+int kk_init_select_ties(kk_handle h, const uint32_t* K, int64_t* out, int64_t capacity, int64_t* n_out,
+                        void* stream) {
+    KK_CHECK_HANDLE(h);
+    if (!K || !n_out) return fail(KK_ERR_ARG, "null argument");
+    return select_ties(h, K, out, capacity, n_out, S(stream));
+}
+
+int kk_init_select_apply(kk_handle h, const uint32_t* K, const int64_t* cut, void* stream) {
+    KK_CHECK_HANDLE(h);
+    if (!K || !cut) return fail(KK_ERR_ARG, "null argument");
+    return select_apply(h, K, cut, S(stream));
+}
+
+int kk_acceptance_table(kk_handle h, uint32_t* out) {
+    if (!h || !out) return fail(KK_ERR_ARG, "null argument");
+    for (int k = 0; k < 7; ++k) out[k] = h->thr[k];
+    return KK_OK;
+}
+
+int kk_words_per_row(kk_handle h, int64_t* w) {
+    if (!h || !w) return fail(KK_ERR_ARG, "null argument");
+    *w = h->g.W;
+    return KK_OK;
+}
+
+int kk_halo_rows(kk_handle h, int64_t* rows) {
+    if (!h || !rows) return fail(KK_ERR_ARG, "null argument");
+    *rows = h->hy;
+    return KK_OK;
+}
+
+int kk_sweep_index(kk_handle h, int64_t* s) {
+    if (!h || !s) return fail(KK_ERR_ARG, "null argument");
+    *s = h->sweep;
+    return KK_OK;
+}
+
+}  // extern "C"

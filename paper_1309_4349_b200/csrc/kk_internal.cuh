@@ -1,0 +1,140 @@
+// kk_internal.cuh — device-side building blocks of the MPKK library.
+//
+// Nothing here is shared with oracle/ (the CPU checker): Philox, geometry and
+// the acceptance table are written independently from the paper, the
+// Random123 definition of Philox and DESIGN.md's readings.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace kk {
+
+// ---------------------------------------------------------------- Philox4x32-10
+// Salmon et al., SC'11 (north_star part 3; R6).  The key schedule
+// only depends on the launch-uniform key, so the compiler keeps it in uniform
+// registers; each round is two 32x32->64 multiplies and two 3-input XORs.
+constexpr uint32_t kPhiloxM0 = 0xD2511F53u;
+constexpr uint32_t kPhiloxM1 = 0xCD9E8D57u;
+constexpr uint32_t kPhiloxW0 = 0x9E3779B9u;
+constexpr uint32_t kPhiloxW1 = 0xBB67AE85u;
+
+struct Words4 {
+    uint32_t a, b, c, d;
+};
+
+__device__ __forceinline__ Words4 philox10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                           uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int round = 0; round < 10; ++round) {
+        const uint32_t lo0 = kPhiloxM0 * c0;
+        const uint32_t hi0 = __umulhi(kPhiloxM0, c0);
+        const uint32_t lo1 = kPhiloxM1 * c2;
+        const uint32_t hi1 = __umulhi(kPhiloxM1, c2);
+        c0 = hi1 ^ c1 ^ k0;
+        c1 = lo1;
+        c2 = hi0 ^ c3 ^ k1;
+        c3 = lo0;
+        k0 += kPhiloxW0;
+        k1 += kPhiloxW1;
+    }
+    return {c0, c1, c2, c3};
+}
+
+// Counter word 3 layout (R6): replica << 8 | tag | iteration.
+constexpr uint32_t kTagSchedule = 0x10u;
+constexpr uint32_t kTagInit = 0x20u;
+
+// ---------------------------------------------------------------- geometry
+// Device lattice layout (include/kk.h): per replica `rows` rows of W uint32
+// words, site x of a row is bit x%32 of word x/32, bits >= Lx are zero.
+struct Geom {
+    int64_t Lx;         // sites per row (multiple of 8)
+    int64_t rows;       // rows held by this handle (slab height)
+    int64_t y_begin;    // global row of local row 0
+    int64_t Ly;         // rows of the full lattice
+    int64_t rep_words;  // words per replica = rows * W
+    int32_t W;          // words per row
+    int32_t tail;       // Lx % 32 (0: last word full)
+    int32_t periodic;   // 1: rows == Ly, rows wrap locally (no halo buffers)
+    int32_t pad;
+};
+
+__device__ __forceinline__ int64_t wrap_mod(int64_t v, int64_t L) {
+    int64_t r = v % L;
+    return r < 0 ? r + L : r;
+}
+
+// Pointer to local row y (may lie in the halo: -hy <= y < rows + hy), or
+// nullptr when the row is outside what this handle can see.
+__device__ __forceinline__ const uint32_t* row_source(const Geom& g, const uint32_t* lat,
+                                                      const uint32_t* halo_top,
+                                                      const uint32_t* halo_bot, int hy,
+                                                      int64_t y) {
+    if (g.periodic) return lat + wrap_mod(y, g.rows) * g.W;
+    if (y >= 0 && y < g.rows) return lat + y * g.W;
+    if (y < 0 && y >= -hy && halo_top) return halo_top + (y + hy) * g.W;
+    if (y >= g.rows && y < g.rows + hy && halo_bot) return halo_bot + (y - g.rows) * g.W;
+    return nullptr;
+}
+
+// The 32 sites p .. p+31 (periodic in Lx) of a packed row, 0 <= p < Lx.
+__device__ __forceinline__ uint32_t get32(const uint32_t* row, int64_t p, const Geom& g) {
+    if (g.Lx < 64) {
+        uint32_t v = 0;
+        int64_t q = p;
+        for (int k = 0; k < 32; ++k) {
+            v |= ((row[q >> 5] >> (q & 31)) & 1u) << k;
+            if (++q == g.Lx) q = 0;
+        }
+        return v;
+    }
+    const int64_t wi = p >> 5;
+    const int sh = (int)(p & 31);
+    const uint32_t lo = row[wi];
+    const uint32_t hi = (wi + 1 < g.W) ? row[wi + 1] : 0u;
+    uint32_t v = sh ? __funnelshift_r(lo, hi, sh) : lo;
+    const int64_t rem = g.Lx - p;
+    if (rem >= 32) return v;
+    v &= (1u << rem) - 1u;
+    return v | (row[0] << rem);
+}
+
+// Valid-bit mask of word gw of a row.
+__device__ __forceinline__ uint32_t word_mask(const Geom& g, int64_t gw) {
+    return (g.tail && gw == g.W - 1) ? ((1u << g.tail) - 1u) : 0xFFFFFFFFu;
+}
+
+// ---------------------------------------------------------------- launch params
+struct PassParams {
+    const uint32_t* src;       // current lattice, replica 0
+    uint32_t* dst;             // next lattice, replica 0
+    const uint32_t* halo_top;  // replica 0 (hy rows per replica) or nullptr
+    const uint32_t* halo_bot;
+    unsigned long long* stats; // [replicas][4]
+    Geom g;
+    int64_t halo_rep_words;    // hy * W
+    int32_t THI, TWI;          // interior tile rows / words
+    int32_t tiles_x;
+    int32_t nA, bA, bB;        // band remap: blockIdx.y < nA -> bA + y, else bB + (y - nA)
+    uint32_t sweep;
+    int32_t j0;                // first iteration of this pass within the sweep
+    uint32_t key0, key1;
+    uint32_t thr[7];           // accept iff u32 <= thr[v+3] (R5)
+};
+
+struct ObsParams {
+    const uint32_t* lat;
+    const uint32_t* halo_bot;  // slab: next slab's first rows, replica stride halo_stride, or nullptr
+    int64_t halo_stride;       // words per replica in halo_bot
+    unsigned long long* out;   // [replicas][2]: N_AB, n_A
+    Geom g;
+    int64_t replicas;
+};
+
+// Cluster sizes below kDense go to a dense per-replica histogram.
+constexpr int kDense = 4096;
+
+// ---------------------------------------------------------------- launch counter
+void count_launch();
+
+}  // namespace kk

@@ -1,0 +1,265 @@
+"""Row-slab multi-GPU driver (north_star: "Large lattices are slab-partitioned by
+rows across the 8 GPUs of one box, with per-phase halo-row exchange via NCCL
+over NVLink overlapped with interior updates").
+
+One process per GPU.  Rank r holds global rows [r*rows, (r+1)*rows) of a
+Lx x (rows*world) periodic lattice.  Every pass (T MPKK iterations, DESIGN.md
+R8) needs hy = 3T rows above and below the slab as they were at the start of
+the pass, so per pass:
+
+    pack_halo (rows [0,hy) and [rows-hy,rows) of the current buffer)
+    exchange  (send top -> previous rank's bottom halo, bottom -> next rank's top halo)
+    interior bands   on a side stream, concurrently with the exchange
+    boundary bands   after the exchange, reading the received halos
+    commit           (flip buffers, advance the (sweep, iteration) counter)
+
+Random numbers are keyed by global coordinates (R6), so the result is
+bit-identical to a single-GPU run of the whole lattice for any world size.
+
+The driver is backend-agnostic: ``GpuSlab`` adapts ``kk.Lattice`` (CUDA,
+device halo buffers, NCCL); tests plug in a CPU backend and a gloo group to
+check the decomposition logic on CPU.
+"""
+from __future__ import annotations
+
+from typing import Optional
+
+import numpy as np
+
+from . import kk
+
+
+# ----------------------------------------------------------------------- comm
+class TorchComm:
+    """torch.distributed plumbing: sums, gathers and the halo exchange."""
+
+    TAG_DOWN, TAG_UP = 11, 12
+
+    def __init__(self, rank: int, world: int, device=None, group=None):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist = torch, dist
+        self.rank, self.world, self.group = rank, world, group
+        self.device = device if device is not None else torch.device("cpu")
+
+    def all_reduce_sum(self, a: np.ndarray) -> np.ndarray:
+        if self.world == 1:
+            return a
+        t = self.torch.from_numpy(np.ascontiguousarray(a, np.int64)).to(self.device)
+        self.dist.all_reduce(t, group=self.group)
+        return t.cpu().numpy()
+
+    def all_gather_rows(self, a: np.ndarray) -> np.ndarray:
+        """Concatenate a (n_i, k) int64 array from every rank (n_i may differ)."""
+        if self.world == 1:
+            return a
+        torch = self.torch
+        n = torch.tensor([a.shape[0]], dtype=torch.int64, device=self.device)
+        ns = [torch.zeros_like(n) for _ in range(self.world)]
+        self.dist.all_gather(ns, n, group=self.group)
+        m = max(int(x.item()) for x in ns)
+        k = a.shape[1]
+        pad = np.zeros((max(m, 1), k), np.int64)
+        pad[: a.shape[0]] = a
+        t = torch.from_numpy(pad).to(self.device)
+        outs = [torch.zeros_like(t) for _ in range(self.world)]
+        self.dist.all_gather(outs, t, group=self.group)
+        return np.concatenate([o.cpu().numpy()[: int(c.item())] for o, c in zip(outs, ns)], axis=0)
+
+    def exchange_start(self, send_top, send_bot, recv_top, recv_bot):
+        """send_top -> rank-1 (its bottom halo); send_bot -> rank+1 (its top halo)."""
+        dist = self.dist
+        prev = (self.rank - 1) % self.world
+        nxt = (self.rank + 1) % self.world
+        ops = [dist.P2POp(dist.isend, send_top, prev, self.group, self.TAG_DOWN),
+               dist.P2POp(dist.irecv, recv_bot, nxt, self.group, self.TAG_DOWN),
+               dist.P2POp(dist.isend, send_bot, nxt, self.group, self.TAG_UP),
+               dist.P2POp(dist.irecv, recv_top, prev, self.group, self.TAG_UP)]
+        return dist.batch_isend_irecv(ops)
+
+    @staticmethod
+    def exchange_wait(works):
+        for w in works:
+            w.wait()
+
+
+# -------------------------------------------------------------- GPU backend
+class GpuSlab:
+    """kk.Lattice + device halo buffers (torch tensors, so NCCL can move them)."""
+
+    def __init__(self, lat: kk.Lattice, device):
+        import torch
+        self.lat = lat
+        self.torch = torch
+        self.device = device
+        self.hy = lat.halo_rows
+        self.replicas = lat.replicas
+
+    def alloc_halo(self):
+        return self.torch.zeros(self.replicas * self.hy * self.lat.W, dtype=self.torch.int32,
+                                device=self.device)
+
+    def pack_halo(self, top, bot, stream):
+        self.lat.pack_halo(top.data_ptr(), bot.data_ptr(), stream)
+
+    def run_pass(self, region, halo_top, halo_bot, stream):
+        self.lat.run_pass(region, None if halo_top is None else halo_top.data_ptr(),
+                          None if halo_bot is None else halo_bot.data_ptr(), stream)
+
+    def commit(self):
+        self.lat.pass_commit()
+
+    def energy(self, halo_bot, stream):
+        return self.lat.energy(None if halo_bot is None else halo_bot.data_ptr(), stream)[0]
+
+    def composition(self, stream):
+        return self.lat.composition(stream)
+
+    def stats(self, reset, stream):
+        return self.lat.stats(reset, stream)
+
+    def cluster_histogram_raw(self, target, stream):
+        return self.lat.cluster_histogram_raw(target, stream=stream)
+
+    def close(self):
+        self.lat.close()
+
+
+# ------------------------------------------------------------- random start
+def select_choose(level: int, hist: np.ndarray, need: np.ndarray, prefix: np.ndarray):
+    """Host bin choice of one radix-select level (mirrors include/kk.h)."""
+    nbins = 1024 if level == 2 else 2048
+    for r in range(hist.shape[0]):
+        c = np.cumsum(hist[r, :nbins])
+        b = int(np.searchsorted(c, need[r], side="left"))
+        b = min(b, nbins - 1)
+        before = int(c[b - 1]) if b > 0 else 0
+        need[r] -= before
+        prefix[r] = (int(prefix[r]) << (10 if level == 2 else 11)) | b
+
+
+def distributed_random_init(lat, comm, fraction_A: float, Lx: int, Ly: int):
+    """Exact-composition random start (R7) over all slabs."""
+    R = lat.replicas
+    nA = int(np.floor(fraction_A * Lx * Ly + 0.5))
+    need = np.full(R, nA, np.int64)
+    prefix = np.zeros(R, np.int64)
+    for level in range(3):
+        h = lat.select_hist(level, None if level == 0 else (prefix & 0xFFFFFFFF).astype(np.uint32))
+        h = comm.all_reduce_sum(h)
+        select_choose(level, h, need, prefix)
+    K = (prefix & 0xFFFFFFFF).astype(np.uint32)
+    ties = comm.all_gather_rows(lat.select_ties(K))
+    cut = np.zeros(R, np.int64)
+    for r in range(R):
+        idx = np.sort(ties[ties[:, 0] == r, 1])
+        assert need[r] <= idx.size, "tie count mismatch"
+        cut[r] = idx[need[r] - 1] + 1 if need[r] > 0 else 0
+    lat.select_apply(K, cut)
+
+
+# ------------------------------------------------------------------ driver
+class SlabDriver:
+    def __init__(self, backend, comm: Optional[TorchComm], rank: int, world: int,
+                 stream=None, side_stream=None):
+        self.be, self.comm, self.rank, self.world = backend, comm, rank, world
+        self.stream, self.side = stream, side_stream
+        if world > 1:
+            self.send_top, self.send_bot = backend.alloc_halo(), backend.alloc_halo()
+            self.recv_top, self.recv_bot = backend.alloc_halo(), backend.alloc_halo()
+
+    def run_pass(self):
+        be = self.be
+        if self.world == 1:
+            be.run_pass(kk.REGION_ALL, None, None, self.stream)
+            be.commit()
+            return
+        be.pack_halo(self.send_top, self.send_bot, self.stream)
+        works = self.comm.exchange_start(self.send_top, self.send_bot, self.recv_top, self.recv_bot)
+        if self.side is not None:
+            self.side.wait_stream(self.stream)
+            be.run_pass(kk.REGION_INTERIOR, None, None, self.side)
+        else:
+            be.run_pass(kk.REGION_INTERIOR, None, None, self.stream)
+        self.comm.exchange_wait(works)
+        be.run_pass(kk.REGION_BOUNDARY, self.recv_top, self.recv_bot, self.stream)
+        if self.side is not None:
+            self.stream.wait_stream(self.side)
+        be.commit()
+
+    def sweep(self, n: int, T: int):
+        for _ in range(n * (16 // T)):
+            self.run_pass()
+
+    def refresh_halos(self):
+        if self.world > 1:
+            self.be.pack_halo(self.send_top, self.send_bot, self.stream)
+            self.comm.exchange_wait(self.comm.exchange_start(self.send_top, self.send_bot,
+                                                             self.recv_top, self.recv_bot))
+
+    def observe(self, ccl: bool = True) -> dict:
+        """N_AB, composition and counters summed over slabs; cluster histogram
+        (single GPU: full lattice)."""
+        self.refresh_halos()
+        nab = np.asarray(self.be.energy(self.recv_bot if self.world > 1 else None, self.stream), np.int64)
+        na = np.asarray(self.be.composition(self.stream), np.int64)
+        st = np.asarray(self.be.stats(True, self.stream), np.int64)
+        if self.world > 1:
+            nab = self.comm.all_reduce_sum(nab)
+            na = self.comm.all_reduce_sum(na)
+            st = self.comm.all_reduce_sum(st)
+        out = {"n_ab": nab.tolist(), "n_a": na.tolist(), "attempted": st[:, 0].tolist(),
+               "trivial": st[:, 1].tolist(), "accepted": st[:, 2].tolist(), "dnab_sum": st[:, 3].tolist()}
+        if ccl and self.world == 1:
+            h = self.be.cluster_histogram_raw(1, self.stream)
+            out["clusters_A"] = int(h[:, 2].sum()) if h.size else 0
+            out["largest_A"] = int(h[:, 1].max()) if h.size else 0
+        return out
+
+
+class Simulation:
+    """What bench.py drives: a full lattice (1 GPU) or one slab of it."""
+
+    def __init__(self, driver: SlabDriver, lat: kk.Lattice, T: int):
+        self.driver, self.lat, self.T = driver, lat, T
+
+    def run_pass(self):
+        self.driver.run_pass()
+
+    def sweep(self, n: int):
+        self.driver.sweep(n, self.T)
+
+    def observe(self, ccl=True):
+        return self.driver.observe(ccl)
+
+    def packed_words(self) -> int:
+        return self.lat.replicas * self.lat.rows * self.lat.W
+
+    def upload_packed(self, host_ptr: int):
+        self.lat.set_packed_ptr(host_ptr, self.driver.stream)
+
+    def download_packed(self, host_ptr: int):
+        import ctypes
+        kk._check(kk.load().kk_get_lattice_packed(self.lat.handle, ctypes.c_void_p(host_ptr),
+                                                  kk.stream_ptr(self.driver.stream)),
+                  "kk_get_lattice_packed")
+
+    def close(self):
+        self.lat.close()
+
+
+def make_simulation(Lx: int, Ly: int, fraction_A: float, omega: float, seed: int, T: int = 4,
+                    world: int = 1, rank: int = 0, device: int = 0, stream=None) -> Simulation:
+    import torch
+    if world == 1:
+        lat = kk.Lattice(Lx, Ly, fraction_A, omega, seed, iters_per_pass=T, device=device)
+        drv = SlabDriver(GpuSlab(lat, torch.device("cuda", device)), None, 0, 1, stream)
+        return Simulation(drv, lat, T)
+    rows = Ly // world
+    lat = kk.Lattice(Lx, Ly, fraction_A, omega, seed, init=kk.KK_INIT_EMPTY, iters_per_pass=T,
+                     y_begin=rank * rows, y_count=rows, device=device)
+    comm = TorchComm(rank, world, torch.device("cuda", device))
+    distributed_random_init(lat, comm, fraction_A, Lx, Ly)
+    side = torch.cuda.Stream(device=device)
+    drv = SlabDriver(GpuSlab(lat, torch.device("cuda", device)), comm, rank, world, stream, side)
+    return Simulation(drv, lat, T)

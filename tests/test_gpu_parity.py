@@ -1,0 +1,235 @@
+"""Parity of the CUDA path (through the C ABI) with the oracle — bit-exact for
+lattice state, N_AB, composition, counters and cluster histograms (north_star:
+"GPU results must match the oracle bit-exactly").
+
+Sizes span several tiles and ragged tails (KK_TWI / KK_THI force small tiles),
+Lx % 32 != 0, all iterations-per-pass settings, replicas, and the BASELINE
+workload sizes (64x64 x 1000 sweeps; 400x400; 4096x4096; the 65536x65536 bench
+lattice via sampled window parity and invariants).
+"""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tests import inputs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1309_4349_b200 import build
+    build.build()
+
+
+def _lat(*a, env=None, **k):
+    from paper_1309_4349_b200 import kk
+    old = {}
+    for key, v in (env or {}).items():
+        old[key] = os.environ.get(key)
+        os.environ[key] = str(v)
+    try:
+        return kk.Lattice(*a, **k)
+    finally:
+        for key, v in old.items():
+            if v is None:
+                os.environ.pop(key, None)
+            else:
+                os.environ[key] = v
+
+
+def _oracle_stats(st):
+    return [st["attempted"], st["trivial"], st["accepted"], st["dnab_sum"]]
+
+
+def test_acceptance_table_matches_oracle_rule():
+    from paper_1309_4349_b200 import kk
+    for om in [0.2, 0.5, 0.6, 1.0, -0.7, 0.0, 3.0]:
+        L = _lat(8, 4, 0.5, om, 1)
+        thr = L.acceptance_table()
+        for v in range(-3, 4):
+            dE = om * 2 * v
+            t = int(thr[v + 3])
+            assert O.metropolis_accept(dE, t)
+            if t < 0xFFFFFFFF:
+                assert not O.metropolis_accept(dE, t + 1)
+        L.close()
+    del kk
+
+
+@pytest.mark.parametrize("Lx,Ly,f,R", [(8, 4, 0.5, 1), (40, 12, 0.3, 1), (64, 64, 0.5, 1),
+                                       (72, 20, 0.7, 2), (400, 400, 0.3, 2), (1024, 36, 0.5, 1)])
+def test_init_random_and_block_parity(Lx, Ly, f, R):
+    from paper_1309_4349_b200 import kk
+    seed = 1000 + Lx
+    L = _lat(Lx, Ly, f, 0.5, seed, replicas=R)
+    got = L.get_lattice()
+    for r in range(R):
+        assert np.array_equal(got[r], O.init_random(Lx, Ly, f, seed, replica=r))
+    assert (L.composition() == O.count_a_for(Lx * Ly, f)).all()
+    B = _lat(Lx, Ly, f, 0.5, seed, replicas=R, init=kk.KK_INIT_BLOCK)
+    gb = B.get_lattice()
+    for r in range(R):
+        assert np.array_equal(gb[r], O.init_block(Lx, Ly, f))
+
+
+def test_set_get_roundtrip_and_observables():
+    for (Lx, Ly) in [(8, 4), (40, 12), (96, 8), (1000, 16)]:
+        a = inputs.random_lattice(Lx, Ly, 0.4, seed=Lx)
+        from paper_1309_4349_b200 import kk
+        L = _lat(Lx, Ly, 0.5, 0.5, 3, init=kk.KK_INIT_EMPTY)
+        L.set_lattice(a[None])
+        assert np.array_equal(L.get_lattice()[0], a)
+        nab, e = L.energy()
+        assert nab[0] == O.n_ab(a)
+        assert e[0] == 0.5 * O.n_ab(a)
+        assert L.composition()[0] == int(a.sum())
+        packed = L.get_packed()
+        assert np.array_equal(inputs.unpack_rows(packed, Lx)[0], a)
+
+
+def _run_parity(Lx, Ly, f, omega, seed, n, T=0, env=None, R=1, start=None):
+    from paper_1309_4349_b200 import kk
+    L = _lat(Lx, Ly, f, omega, seed, replicas=R, iters_per_pass=T, env=env,
+             init=kk.KK_INIT_EMPTY if start is not None else kk.KK_INIT_RANDOM)
+    if start is not None:
+        L.set_lattice(start)
+        ref = [start[r].copy() for r in range(R)]
+    else:
+        ref = [O.init_random(Lx, Ly, f, seed, replica=r) for r in range(R)]
+    nab0 = L.energy()[0]
+    L.sweep(n)
+    got = L.get_lattice()
+    st = L.stats()
+    nab1 = L.energy()[0]
+    for r in range(R):
+        ost = O.run(ref[r], omega, seed, n, replica=r)
+        assert np.array_equal(got[r], ref[r]), f"lattice mismatch replica {r}"
+        assert list(st[r]) == _oracle_stats(ost)
+        assert nab1[r] == O.n_ab(ref[r])
+        assert nab1[r] - nab0[r] == st[r][3]
+    assert (L.composition() == [int(x.sum()) for x in ref]).all()
+    return L, ref
+
+
+def test_config0_64x64_1000_sweeps():
+    """BASELINE configs[0]: 64x64, 50:50, omega=0.5, 1000 sweeps, fixed seed."""
+    _run_parity(64, 64, 0.5, 0.5, 20240601, 1000)
+
+
+@pytest.mark.parametrize("T", [1, 2, 4, 8])
+def test_iters_per_pass_all_equal_oracle(T):
+    _run_parity(96, 40, 0.5, 0.6, 77, 12, T=T)
+
+
+@pytest.mark.parametrize("Lx,Ly,env", [
+    (8, 4, None), (16, 8, None), (40, 12, None), (72, 20, None),
+    (200, 52, {"KK_TWI": 2, "KK_THI": 16}),      # many tiles, ragged last tile (W=7)
+    (1000, 44, {"KK_TWI": 5, "KK_THI": 12}),     # Lx % 32 = 8, ragged in x and y
+    (2048, 64, {"KK_TWI": 16, "KK_THI": 20}),
+])
+def test_sweep_parity_shapes(Lx, Ly, env):
+    _run_parity(Lx, Ly, 0.5, 0.7, Lx * 31 + Ly, 6, env=env)
+
+
+@pytest.mark.parametrize("omega", [0.0, 0.2, 1.0, -0.5, 4.0])
+def test_sweep_parity_omega(omega):
+    _run_parity(128, 32, 0.3, omega, 5, 10)
+
+
+def test_replicas_and_arbitrary_start():
+    start = inputs.random_lattice(64, 24, 0.45, seed=9, replicas=3)
+    _run_parity(64, 24, 0.5, 0.8, 4242, 15, R=3, start=start)
+    stripes = np.stack([inputs.striped_lattice(48, 16)] * 2)
+    _run_parity(48, 16, 0.5, 1.0, 17, 20, R=2, start=stripes)
+
+
+def test_degenerate_lattices():
+    from paper_1309_4349_b200 import kk
+    for f in (0.0, 1.0):
+        L = _lat(32, 8, f, 0.5, 1)
+        before = L.get_lattice()
+        L.sweep(3)
+        assert np.array_equal(L.get_lattice(), before)
+        st = L.stats()[0]
+        assert st[0] == 3 * 256 and st[1] == 3 * 256 and st[2] == 0
+        assert L.energy()[0][0] == 0
+        hist = L.cluster_histogram(1)[0]
+        assert hist == ([(256, 1)] if f == 1.0 else [])
+    L = _lat(32, 8, 0.5, 0.5, 1, init=kk.KK_INIT_EMPTY)
+    L.sweep(0)
+    assert L.sweep_index() == 0
+
+
+@pytest.mark.parametrize("Lx,Ly,R", [(64, 64, 1), (400, 400, 2), (40, 12, 3)])
+def test_cluster_histogram_parity(Lx, Ly, R):
+    L, ref = _run_parity(Lx, Ly, 0.5, 0.9, 31, 20 if Lx < 400 else 5, R=R)
+    for target in (0, 1):
+        got = L.cluster_histogram(target)
+        for r in range(R):
+            assert got[r] == O.cluster_histogram(ref[r], target)
+
+
+def test_cluster_histogram_large_clusters():
+    """Sizes >= 4096 go through the big-cluster list: all-A, half-plane."""
+    from paper_1309_4349_b200 import kk
+    a = np.zeros((2, 128, 128), np.uint8)
+    a[0] = 1
+    a[1, :64] = 1
+    a[1, 100, 5] = 1
+    L = _lat(128, 128, 0.5, 0.5, 1, replicas=2, init=kk.KK_INIT_EMPTY)
+    L.set_lattice(a)
+    got = L.cluster_histogram(1)
+    assert got[0] == [(128 * 128, 1)]
+    assert got[1] == O.cluster_histogram(a[1], 1) == [(1, 1), (64 * 128, 1)]
+
+
+def test_config1_400x400_paper_size():
+    """BASELINE configs[1] shapes: 400x400 at 50:50 and 30:70 compositions."""
+    for f, om in [(0.5, 0.6), (0.3, 1.0)]:
+        L, ref = _run_parity(400, 400, f, om, 400, 3)
+        assert L.cluster_histogram(1)[0] == O.cluster_histogram(ref[0], 1)
+
+
+def test_config2_4096x4096_one_sweep():
+    """BASELINE configs[2]: the single-B200 throughput lattice, full parity."""
+    _run_parity(4096, 4096, 0.5, 0.6, 123, 1)
+
+
+def test_bench_lattice_65536_window_and_invariants():
+    """BASELINE configs[4] lattice (65536 x 65536, what bench.py times):
+    invariants over the whole lattice + sampled window parity for one pass."""
+    from paper_1309_4349_b200 import kk
+    Lx = Ly = 65536
+    L = _lat(Lx, Ly, 0.5, 0.6, 99, init=kk.KK_INIT_BLOCK)
+    nA = L.composition()[0]
+    assert nA == Lx * Ly // 2
+    L.sweep(1)                                    # mix the block start
+    nab0 = L.energy()[0][0]
+    L.stats(reset=True)
+    T = 4
+    hy = 3 * T
+    before = L.get_packed()[0]
+    s = L.sweep_index()
+    L.run_pass(kk.REGION_ALL, None, None)         # iterations 0..3 of sweep s
+    L.pass_commit()
+    after = L.get_packed()[0]
+    st = L.stats()[0]
+    nab1 = L.energy()[0][0]
+    assert L.composition()[0] == nA
+    assert nab1 - nab0 == st[3]
+    assert st[0] == Lx * Ly // 4                 # T=4 iterations x N/16 centres
+    rng = np.random.default_rng(5)
+    for y0 in [0, Ly - 8, int(rng.integers(16, Ly - 16))]:
+        H = 8
+        rows = [(y0 - hy + r) % Ly for r in range(H + 2 * hy)]
+        win = np.ascontiguousarray(inputs.unpack_rows(before[rows], Lx))
+        O.window_iterations(win, Ly, y0 - hy, 0.6, 99, s, 0, 0, T, hy, hy + H)
+        exp = win[hy:hy + H]
+        got = inputs.unpack_rows(after[[(y0 + r) % Ly for r in range(H)]], Lx)
+        assert np.array_equal(got, exp)
