@@ -65,7 +65,7 @@ typedef struct {
     double omega_kT;        /* omega_AB / kT, finite */
     uint64_t seed;          /* Philox key (R6) */
     int32_t init_mode;      /* kk_init_mode */
-    int32_t iters_per_pass; /* T in {1,2,4,8}: MPKK iterations fused per HBM pass; 0 = default (4) */
+    int32_t iters_per_pass; /* T in {1,2,4,8}: MPKK iterations fused per HBM pass; 0 = default (8) */
     int32_t device;         /* CUDA device ordinal; -1 = current */
     int32_t reserved;
 } kk_config;

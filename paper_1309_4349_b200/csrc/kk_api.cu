@@ -33,10 +33,12 @@ cudaError_t launch_pack(const uint8_t* bytes, uint32_t* lat, const Geom& g, int6
 cudaError_t launch_unpack(const uint32_t* lat, uint8_t* bytes, const Geom& g, int64_t replicas, cudaStream_t s);
 cudaError_t launch_pack_halo(const uint32_t* lat, uint32_t* top, uint32_t* bot, const Geom& g, int64_t replicas,
                              int hy, cudaStream_t s);
-template <typename L>
-cudaError_t launch_ccl(const uint32_t* lat, const Geom& g, int64_t replicas, int target, L* lab, L* cnt,
-                       unsigned int* hist, unsigned long long* big, unsigned long long* nbig, int64_t big_cap,
-                       cudaStream_t s);
+int64_t ccl_edge_entries(const Geom& g, int64_t replicas);
+int64_t ccl_node_cap(const Geom& g, int64_t replicas);
+cudaError_t launch_ccl(const uint32_t* lat, const Geom& g, int64_t replicas, int target, uint32_t* edges,
+                       uint32_t* node_size, uint32_t* node_par, uint32_t* node_rep,
+                       unsigned long long* root_size, unsigned int* counter, unsigned int* hist,
+                       unsigned long long* big, unsigned long long* nbig, int64_t big_cap, cudaStream_t s);
 
 }  // namespace kk
 
@@ -57,10 +59,13 @@ struct kk_lattice {
     int64_t sweep = 0;
     int j = 0;
     int THI = 0, TWI = 0, tiles_x = 0, bands = 0, b_lo = 0, b_hi = 0;
-    // cluster analysis (lazy)
-    void* lab = nullptr;
-    void* cnt = nullptr;
-    int lab64 = 0;
+    // cluster analysis workspace (lazy)
+    uint32_t* edges = nullptr;
+    uint32_t* node_size = nullptr;
+    uint32_t* node_par = nullptr;
+    uint32_t* node_rep = nullptr;
+    unsigned long long* root_size = nullptr;
+    unsigned int* counter = nullptr;
     unsigned int* hist = nullptr;
     unsigned long long* big = nullptr;
     unsigned long long* nbig = nullptr;
@@ -116,8 +121,8 @@ void make_thresholds(double omega, uint32_t thr[7]) {
 }
 
 void choose_tiles(kk_lattice* h) {
-    const int twi_t = std::max(1, env_int("KK_TWI", 64));
-    const int thi_t = std::max(4, env_int("KK_THI", 256));
+    const int twi_t = std::max(1, env_int("KK_TWI", 62));
+    const int thi_t = std::max(4, env_int("KK_THI", 160));
     const int64_t W = h->g.W, rows = h->g.rows;
     const int64_t nx = (W + twi_t - 1) / twi_t;
     h->TWI = (int)((W + nx - 1) / nx);
@@ -151,6 +156,10 @@ PassParams make_pass_params(kk_lattice* h, const uint32_t* ht, const uint32_t* h
     P.j0 = h->j;
     P.key0 = (uint32_t)(h->seed & 0xFFFFFFFFu);
     P.key1 = (uint32_t)(h->seed >> 32);
+    for (int r = 0; r < 10; ++r) {
+        P.rk[r] = P.key0 + (uint32_t)r * 0x9E3779B9u;
+        P.rk[10 + r] = P.key1 + (uint32_t)r * 0xBB67AE85u;
+    }
     for (int k = 0; k < 7; ++k) P.thr[k] = h->thr[k];
     return P;
 }
@@ -179,8 +188,12 @@ void free_all(kk_lattice* h) {
     cudaFree(h->buf[1]);
     cudaFree(h->stats);
     cudaFree(h->obs);
-    cudaFree(h->lab);
-    cudaFree(h->cnt);
+    cudaFree(h->edges);
+    cudaFree(h->node_size);
+    cudaFree(h->node_par);
+    cudaFree(h->node_rep);
+    cudaFree(h->root_size);
+    cudaFree(h->counter);
     cudaFree(h->hist);
     cudaFree(h->big);
     cudaFree(h->nbig);
@@ -330,7 +343,7 @@ int kk_create_ex(kk_handle* out, const kk_config* c) {
     if (c->replicas < 1 || c->replicas >= (1 << 16)) return fail(KK_ERR_ARG, "replicas must be in [1, 65535]");
     if (!(c->fraction_A >= 0.0 && c->fraction_A <= 1.0)) return fail(KK_ERR_ARG, "fraction_A must be in [0,1]");
     if (!std::isfinite(c->omega_kT)) return fail(KK_ERR_ARG, "omega_kT must be finite");
-    const int T = c->iters_per_pass ? c->iters_per_pass : env_int("KK_T", 4);
+    const int T = c->iters_per_pass ? c->iters_per_pass : env_int("KK_T", 8);
     if (T != 1 && T != 2 && T != 4 && T != 8) return fail(KK_ERR_ARG, "iters_per_pass must be 1, 2, 4 or 8");
     if (c->init_mode < 0 || c->init_mode > 2) return fail(KK_ERR_ARG, "bad init_mode");
     const bool slab = c->y_count != c->Ly;
@@ -521,38 +534,24 @@ int kk_cluster_histogram(kk_handle h, int target, int64_t* out, int64_t capacity
     if (!n_out) return fail(KK_ERR_ARG, "n_out is null");
     if (!h->g.periodic) return fail(KK_ERR_STATE, "cluster histogram needs a full-lattice handle");
     cudaStream_t s = S(stream);
-    const int64_t N = h->g.Lx * h->g.rows;
-    const int64_t n = N * h->R;
-    const bool need64 = N >= (int64_t)0xFFFFFFFFll;
-    if (!h->lab || (need64 != (bool)h->lab64)) {
-        cudaFree(h->lab);
-        cudaFree(h->cnt);
-        cudaFree(h->hist);
-        cudaFree(h->big);
-        cudaFree(h->nbig);
-        h->lab = h->cnt = nullptr;
-        h->hist = nullptr;
-        h->big = h->nbig = nullptr;
-        const size_t ls = need64 ? 8 : 4;
-        h->lab64 = need64;
+    const int64_t n = h->g.Lx * h->g.rows * h->R;
+    if (!h->edges) {
+        const int64_t ne = ccl_edge_entries(h->g, h->R), nn = ccl_node_cap(h->g, h->R);
         h->big_cap = n / kDense + 16;
-        if (cudaMalloc(&h->lab, ls * n) || cudaMalloc(&h->cnt, ls * n) ||
+        if (cudaMalloc(&h->edges, 4 * ne) || cudaMalloc(&h->node_size, 4 * nn) ||
+            cudaMalloc(&h->node_par, 4 * nn) || cudaMalloc(&h->node_rep, 4 * nn) ||
+            cudaMalloc(&h->root_size, 8 * nn) || cudaMalloc(&h->counter, sizeof(unsigned int)) ||
             cudaMalloc(&h->hist, sizeof(unsigned int) * kDense * h->R) ||
             cudaMalloc(&h->big, sizeof(unsigned long long) * 2 * h->big_cap) ||
             cudaMalloc(&h->nbig, sizeof(unsigned long long))) {
             cudaGetLastError();
-            return fail(KK_ERR_NOMEM, "cluster buffers: device allocation failed");
+            return fail(KK_ERR_NOMEM, "cluster workspace: device allocation failed");
         }
     }
     KK_CUDA(cudaMemsetAsync(h->hist, 0, sizeof(unsigned int) * kDense * h->R, s));
     KK_CUDA(cudaMemsetAsync(h->nbig, 0, sizeof(unsigned long long), s));
-    if (h->lab64) {
-        KK_CUDA(launch_ccl<unsigned long long>(h->buf[h->cur], h->g, h->R, target, (unsigned long long*)h->lab,
-                                               (unsigned long long*)h->cnt, h->hist, h->big, h->nbig, h->big_cap, s));
-    } else {
-        KK_CUDA(launch_ccl<uint32_t>(h->buf[h->cur], h->g, h->R, target, (uint32_t*)h->lab, (uint32_t*)h->cnt,
-                                     h->hist, h->big, h->nbig, h->big_cap, s));
-    }
+    KK_CUDA(launch_ccl(h->buf[h->cur], h->g, h->R, target, h->edges, h->node_size, h->node_par, h->node_rep,
+                       h->root_size, h->counter, h->hist, h->big, h->nbig, h->big_cap, s));
     std::vector<unsigned int> hist((size_t)kDense * h->R);
     unsigned long long nb = 0;
     KK_CUDA(cudaMemcpyAsync(hist.data(), h->hist, sizeof(unsigned int) * kDense * h->R, cudaMemcpyDeviceToHost, s));

@@ -1,151 +1,277 @@
 // kk_ccl.cu — GPU connected-component labelling and cluster-size histogram
 // ("Cluster Analysis methods", Figs. 9-11; R9).
 //
-// The paper labels clusters with Hoshen-Kopelman (a sequential union-find
-// sweep).  On the GPU the same union-find runs concurrently: every target site
-// hooks itself to its three forward neighbours (+1,0) (0,+1) (+1,+1) with
-// lock-free CAS linking of the larger root under the smaller one (parents
-// always have smaller indices, so every component's final root is its
-// smallest site index — the result is independent of thread scheduling), then
-// labels are flattened, sizes counted with warp-aggregated atomics, and the
-// roots' sizes binned: sizes < kDense into a dense per-replica histogram, the
-// rare larger clusters appended to a list.
+// The paper uses Hoshen-Kopelman: a sequential raster sweep with union-find
+// label merging.  On the GPU the lattice is cut into tiles (kTR rows x
+// kTW words) and the cluster multiset is built in three phases:
+//
+//  1. tile kernel (shared memory): load the tile's bits, union-find over the
+//     six-neighbour bonds that stay inside the tile (32-bit labels, shared
+//     memory CAS), count each local component's size.  Components that touch no
+//     tile edge are complete: their sizes go straight into the histogram.
+//     Edge-touching components become global "nodes" (size recorded) and the
+//     tile writes the node id of every edge site.
+//  2. merge kernel: for every bond crossing a tile boundary (periodic
+//     lattice), union the two nodes in a global union-find (CAS linking of the
+//     larger root under the smaller).
+//  3. node kernels: flatten, sum node sizes per root (64-bit), histogram the
+//     roots.
+//
+// Global traffic is one bit per site plus the tile edges, instead of a
+// 4-8 byte label per site.  The resulting multiset is unique, so the output
+// does not depend on scheduling.
 #include "kk_internal.cuh"
 
 namespace kk {
 
 namespace {
 
-template <typename L>
-struct LabelTraits;
-template <>
-struct LabelTraits<uint32_t> {
-    static constexpr uint32_t none = 0xFFFFFFFFu;
+constexpr int kTR = 32;                    // tile rows
+constexpr int kTW = 8;                     // tile words per row (256 sites)
+constexpr int kTX = 32 * kTW;              // tile sites per row
+constexpr int kSites = kTR * kTX;          // 8192
+constexpr int kEdge = 2 * kTX + 2 * kTR;   // edge entries per tile
+constexpr int kThreads = 512;
+constexpr uint32_t kNone = 0xFFFFFFFFu;
+// 32-bit labels in shared memory: sub-word CAS is emulated by a CAS loop on the
+// containing word, which races with the plain 16-bit stores of path halving.
+
+__device__ __forceinline__ uint32_t find32(uint32_t* par, uint32_t v) {
+    volatile uint32_t* vp = par;
+    uint32_t cur = vp[v];
+    while (cur != v) {
+        const uint32_t nxt = vp[cur];
+        if (nxt != cur) vp[v] = nxt;
+        v = cur;
+        cur = nxt;
+    }
+    return v;
+}
+
+// Read-only root walk: used once all unions are done, while other threads
+// overwrite their own entries with final roots (a path-halving write here
+// could replace such a final root with a lower ancestor).
+__device__ __forceinline__ uint32_t root_of(const uint32_t* par, uint32_t v) {
+    const volatile uint32_t* vp = par;
+    uint32_t cur = vp[v];
+    while (cur != v) {
+        v = cur;
+        cur = vp[v];
+    }
+    return v;
+}
+
+__device__ __forceinline__ void union32(uint32_t* par, uint32_t a, uint32_t b) {
+    a = find32(par, a);
+    b = find32(par, b);
+    while (a != b) {
+        if (a < b) {
+            const uint32_t t = a;
+            a = b;
+            b = t;
+        }
+        const uint32_t old = atomicCAS(par + a, a, b);
+        if (old == a) return;
+        a = find32(par, old);
+        b = find32(par, b);
+    }
+}
+
+struct CclParams {
+    const uint32_t* lat;
+    Geom g;
+    int target;
+    int tiles_x, tiles_y;          // per replica
+    uint32_t* edges;               // [tile][kEdge]: top[kTX] bottom[kTX] left[kTR] right[kTR]
+    uint32_t* node_size;           // [node]
+    uint32_t* node_par;            // [node]
+    uint32_t* node_rep;            // [node] replica of the node
+    unsigned long long* root_size; // [node]
+    unsigned int* node_count;      // device counter
+    unsigned int* hist;            // [replica][kDense]
+    unsigned long long* big;       // (replica, size) pairs
+    unsigned long long* nbig;
+    int64_t big_cap;
+    int64_t node_cap;
 };
-template <>
-struct LabelTraits<unsigned long long> {
-    static constexpr unsigned long long none = ~0ull;
-};
 
-__device__ __forceinline__ bool site_bit(const uint32_t* lat, const Geom& g, int64_t x, int64_t y) {
-    return (lat[y * g.W + (x >> 5)] >> (x & 31)) & 1u;
-}
-
-template <typename L>
-__device__ __forceinline__ L find_root(L* lab, L v) {
-    volatile L* vl = lab;
-    L cur = vl[v];
-    if (cur != v) {
-        L prev = v, next;
-        while (cur > (next = vl[cur])) {  // path halving; parents are smaller
-            vl[prev] = next;
-            prev = cur;
-            cur = next;
+__device__ __forceinline__ void hist_add(const CclParams& P, int64_t rep, unsigned long long s) {
+    if (s < (unsigned long long)kDense) {
+        atomicAdd(P.hist + rep * kDense + s, 1u);
+    } else {
+        const unsigned long long slot = atomicAdd(P.nbig, 1ull);
+        if ((int64_t)slot < P.big_cap) {
+            P.big[2 * slot] = (unsigned long long)rep;
+            P.big[2 * slot + 1] = s;
         }
     }
-    return cur;
 }
 
-template <typename L>
-__global__ void ccl_init_kernel(const uint32_t* lat, L* lab, Geom g, int64_t replicas, int target) {
-    const int64_t N = g.rows * g.Lx;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N * replicas;
+// ---- phase 1: one CTA per tile ------------------------------------------------
+__global__ void __launch_bounds__(kThreads) ccl_tile_kernel(const CclParams P) {
+    extern __shared__ uint32_t smem[];
+    uint32_t* bits = smem;                                            // [kTR*kTW]
+    uint32_t* cnt = bits + kTR * kTW;                                 // [kSites/2] two 16-bit counters/word
+    uint32_t* touch = cnt + kSites / 2;                               // [kSites/32] edge-touch flag per root
+    uint32_t* lab = touch + kSites / 32;                              // [kSites]
+    uint16_t* node_s = reinterpret_cast<uint16_t*>(lab + kSites);     // [kEdge] sizes of edge nodes
+    __shared__ unsigned int n_nodes, node_base;
+
+    const Geom& g = P.g;
+    const int tx = blockIdx.x, ty = blockIdx.y;
+    const int64_t rep = blockIdx.z;
+    const int64_t X0 = (int64_t)tx * kTX, Y0 = (int64_t)ty * kTR;
+    const int w_tile = (int)min64(kTX, g.Lx - X0);    // valid sites per row
+    const int h_tile = (int)min64(kTR, g.rows - Y0);  // valid rows
+    const uint32_t* lat = P.lat + rep * g.rep_words;
+    const uint32_t tmask = P.target ? 0u : 0xFFFFFFFFu;
+
+    if (threadIdx.x == 0) n_nodes = 0;
+    for (int i = threadIdx.x; i < kTR * kTW; i += kThreads) {
+        const int r = i / kTW, w = i - r * kTW;
+        uint32_t v = 0;
+        if (r < h_tile && 32 * w < w_tile) {
+            const int64_t gw = X0 / 32 + w;
+            v = (lat[(Y0 + r) * g.W + gw] ^ tmask);         // 1 = target site
+            const int nv = w_tile - 32 * w;
+            if (nv < 32) v &= (1u << nv) - 1u;
+        }
+        bits[i] = v;
+    }
+    for (int i = threadIdx.x; i < kSites / 2; i += kThreads) cnt[i] = 0;
+    for (int i = threadIdx.x; i < kSites / 32; i += kThreads) touch[i] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < kSites; i += kThreads) {
+        const bool t = (bits[i >> 5] >> (i & 31)) & 1u;
+        lab[i] = t ? (uint32_t)i : kNone;
+    }
+    __syncthreads();
+    // unions over in-tile bonds (+1,0) (0,+1) (+1,+1)
+    for (int i = threadIdx.x; i < kSites; i += kThreads) {
+        if (!((bits[i >> 5] >> (i & 31)) & 1u)) continue;
+        const int r = i / kTX, x = i - r * kTX;
+        if (x + 1 < w_tile && ((bits[(i + 1) >> 5] >> ((i + 1) & 31)) & 1u)) union32(lab, i, i + 1);
+        if (r + 1 < h_tile) {
+            const int j = i + kTX;
+            if ((bits[j >> 5] >> (j & 31)) & 1u) union32(lab, i, j);
+            if (x + 1 < w_tile && ((bits[(j + 1) >> 5] >> ((j + 1) & 31)) & 1u)) union32(lab, i, j + 1);
+        }
+    }
+    __syncthreads();
+    // flatten, count, mark edge-touching roots
+    for (int i = threadIdx.x; i < kSites; i += kThreads) {
+        if (lab[i] == kNone) continue;
+        const uint32_t root = root_of(lab, (uint32_t)i);
+        lab[i] = root;
+        atomicAdd(&cnt[root >> 1], 1u << (16 * (root & 1)));
+        const int r = i / kTX, x = i - r * kTX;
+        if (r == 0 || r == h_tile - 1 || x == 0 || x == w_tile - 1) atomicOr(&touch[root >> 5], 1u << (root & 31));
+    }
+    __syncthreads();
+    // complete components -> histogram; edge components -> local node index
+    uint16_t* cnt16 = reinterpret_cast<uint16_t*>(cnt);
+    for (int i = threadIdx.x; i < kSites; i += kThreads) {
+        if (lab[i] != (uint32_t)i) continue;
+        const uint32_t s = cnt16[i];
+        if ((touch[i >> 5] >> (i & 31)) & 1u) {
+            const unsigned int k = atomicAdd(&n_nodes, 1u);
+            node_s[k] = (uint16_t)s;
+            cnt16[i] = (uint16_t)k;   // root -> local node index (this thread owns this half)
+        } else {
+            hist_add(P, rep, s);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) node_base = atomicAdd(P.node_count, n_nodes);
+    __syncthreads();
+    const unsigned int base = node_base;
+    for (unsigned int k = threadIdx.x; k < n_nodes; k += kThreads) {
+        if ((int64_t)(base + k) < P.node_cap) {
+            P.node_size[base + k] = node_s[k];
+            P.node_par[base + k] = base + k;
+            P.node_rep[base + k] = (uint32_t)rep;
+            P.root_size[base + k] = 0ull;
+        }
+    }
+    // edge export
+    const int64_t tile = (rep * P.tiles_y + ty) * P.tiles_x + tx;
+    uint32_t* E = P.edges + tile * kEdge;
+    auto node_of = [&](int r, int x) -> uint32_t {
+        if (r >= h_tile || x >= w_tile) return kNone;
+        const uint32_t l = lab[r * kTX + x];
+        return l == kNone ? kNone : base + cnt16[l];
+    };
+    for (int e = threadIdx.x; e < kEdge; e += kThreads) {
+        uint32_t v;
+        if (e < kTX) v = node_of(0, e);                                   // top row
+        else if (e < 2 * kTX) v = node_of(h_tile - 1, e - kTX);           // bottom row
+        else if (e < 2 * kTX + kTR) v = node_of(e - 2 * kTX, 0);          // left column
+        else v = node_of(e - 2 * kTX - kTR, w_tile - 1);                  // right column
+        E[e] = v;
+    }
+}
+
+// ---- phase 2: unions across tile boundaries -----------------------------------
+__global__ void ccl_merge_kernel(const CclParams P) {
+    const Geom& g = P.g;
+    const int64_t ntiles = (int64_t)P.tiles_x * P.tiles_y;
+    const int64_t rep = blockIdx.y;
+    const int64_t per_tile = kTR + kTX;  // right-column sites + bottom-row sites
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ntiles * per_tile;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = i / N, k = i - r * N;
-        const int64_t y = k / g.Lx, x = k - y * g.Lx;
-        const bool t = site_bit(lat + r * g.rep_words, g, x, y) == (target != 0);
-        lab[i] = t ? (L)k : LabelTraits<L>::none;
-    }
-}
-
-template <typename L>
-__global__ void ccl_hook_kernel(const uint32_t* lat, L* lab, Geom g, int64_t replicas, int target) {
-    const int64_t N = g.rows * g.Lx;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N * replicas;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = i / N, k = i - r * N;
-        L* rl = lab + r * N;
-        if (rl[k] == LabelTraits<L>::none) continue;
-        const int64_t y = k / g.Lx, x = k - y * g.Lx;
-        const int64_t x1 = (x + 1 == g.Lx) ? 0 : x + 1;
-        const int64_t y1 = (y + 1 == g.rows) ? 0 : y + 1;
-        const int64_t nb[3] = {y * g.Lx + x1, y1 * g.Lx + x, y1 * g.Lx + x1};
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-            const int64_t o = nb[d];
-            if (rl[o] == LabelTraits<L>::none) continue;
-            L a = find_root<L>(rl, (L)k);
-            L b = find_root<L>(rl, (L)o);
-            while (a != b) {
-                if (a < b) {
-                    const L old = atomicCAS(rl + b, b, a);
-                    if (old == b) break;
-                    b = old;
-                } else {
-                    const L old = atomicCAS(rl + a, a, b);
-                    if (old == a) break;
-                    a = old;
-                }
-            }
+        const int64_t t = i / per_tile;
+        const int e = (int)(i - t * per_tile);
+        const int ty = (int)(t / P.tiles_x), tx = (int)(t - (int64_t)ty * P.tiles_x);
+        const int64_t X0 = (int64_t)tx * kTX, Y0 = (int64_t)ty * kTR;
+        const int w_tile = (int)min64(kTX, g.Lx - X0);
+        const int h_tile = (int)min64(kTR, g.rows - Y0);
+        const int txr = (tx + 1 == P.tiles_x) ? 0 : tx + 1;
+        const int tyb = (ty + 1 == P.tiles_y) ? 0 : ty + 1;
+        const uint32_t* E = P.edges + ((rep * P.tiles_y + ty) * P.tiles_x + tx) * kEdge;
+        const uint32_t* Er = P.edges + ((rep * P.tiles_y + ty) * P.tiles_x + txr) * kEdge;
+        const uint32_t* Eb = P.edges + ((rep * P.tiles_y + tyb) * P.tiles_x + tx) * kEdge;
+        const uint32_t* Ed = P.edges + ((rep * P.tiles_y + tyb) * P.tiles_x + txr) * kEdge;
+        if (e < kTR) {  // right column row e: bonds (+1,0) and (+1,+1)
+            if (e >= h_tile) continue;
+            const uint32_t a = E[2 * kTX + kTR + e];
+            if (a == kNone) continue;
+            const uint32_t b = Er[2 * kTX + e];                       // (X1, y) = left col of right tile
+            if (b != kNone) union32(P.node_par, a, b);
+            const uint32_t c = (e + 1 < h_tile) ? Er[2 * kTX + e + 1]  // (X1, y+1)
+                                                : Ed[2 * kTX + 0];     // wraps into the diagonal tile
+            if (c != kNone) union32(P.node_par, a, c);
+        } else {        // bottom row site x: bonds (0,+1) and (+1,+1)
+            const int x = e - kTR;
+            if (x >= w_tile) continue;
+            const uint32_t a = E[kTX + x];
+            if (a == kNone) continue;
+            const uint32_t b = Eb[x];                                  // (x, Y1) top row of tile below
+            if (b != kNone) union32(P.node_par, a, b);
+            const uint32_t c = (x + 1 < w_tile) ? Eb[x + 1] : Ed[0];   // (x+1, Y1)
+            if (c != kNone) union32(P.node_par, a, c);
         }
     }
 }
 
-template <typename L>
-__global__ void ccl_flatten_count_kernel(L* lab, L* cnt, Geom g, int64_t replicas) {
-    const int64_t N = g.rows * g.Lx;
-    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < N * replicas;
-         i0 += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = i0 + threadIdx.x;
-        unsigned long long key = ~0ull;
-        if (i < N * replicas) {
-            const int64_t r = i / N, k = i - r * N;
-            L* rl = lab + r * N;
-            if (rl[k] != LabelTraits<L>::none) {
-                const L root = find_root<L>(rl, (L)k);
-                rl[k] = root;
-                key = (unsigned long long)(r * N + (int64_t)root);
-            }
-        }
-        const unsigned mask = __match_any_sync(0xFFFFFFFFu, key);
-        if (key != ~0ull && (threadIdx.x & 31) == __ffs(mask) - 1)
-            atomicAdd(cnt + key, (L)__popc(mask));
+// ---- phase 3: flatten + sum sizes per root, then histogram roots ----------------
+__global__ void ccl_nodes_sum_kernel(const CclParams P) {
+    const unsigned int n = (unsigned int)min64((int64_t)*P.node_count, P.node_cap);
+    for (unsigned int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t r = find32(P.node_par, i);
+        atomicAdd(P.root_size + r, (unsigned long long)P.node_size[i]);
     }
 }
 
-template <typename L>
-__global__ void ccl_hist_kernel(const L* lab, const L* cnt, Geom g, int64_t replicas,
-                                unsigned int* hist, unsigned long long* big, unsigned long long* nbig,
-                                int64_t big_cap) {
-    const int64_t N = g.rows * g.Lx;
-    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < N * replicas;
-         i0 += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = i0 + threadIdx.x;
-        unsigned long long key = ~0ull;
-        int64_t r = 0;
-        unsigned long long s = 0;
-        if (i < N * replicas) {
-            r = i / N;
-            const int64_t k = i - r * N;
-            if (lab[i] == (L)k) {  // root of its cluster
-                s = (unsigned long long)cnt[i];
-                if (s < (unsigned long long)kDense) {
-                    key = (unsigned long long)r * kDense + s;
-                } else {
-                    const unsigned long long slot = atomicAdd(nbig, 1ull);
-                    if ((int64_t)slot < big_cap) {
-                        big[2 * slot] = (unsigned long long)r;
-                        big[2 * slot + 1] = s;
-                    }
-                }
-            }
-        }
-        const unsigned mask = __match_any_sync(0xFFFFFFFFu, key);
-        if (key != ~0ull && (threadIdx.x & 31) == __ffs(mask) - 1) atomicAdd(hist + key, (unsigned)__popc(mask));
+// replica-aware variant: node_rep[i] gives the replica of node i
+__global__ void ccl_nodes_hist_rep_kernel(const CclParams P, const uint32_t* node_rep) {
+    const unsigned int n = (unsigned int)min64((int64_t)*P.node_count, P.node_cap);
+    for (unsigned int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        if (P.node_par[i] != i) continue;
+        hist_add(P, node_rep ? node_rep[i] : 0, P.root_size[i]);
     }
 }
 
-int grid_ccl(int64_t n) {
+int grid_for_n(int64_t n) {
     int64_t b = (n + 255) / 256;
     if (b > 148 * 16) b = 148 * 16;
     return (int)(b < 1 ? 1 : b);
@@ -153,28 +279,57 @@ int grid_ccl(int64_t n) {
 
 }  // namespace
 
-template <typename L>
-cudaError_t launch_ccl(const uint32_t* lat, const Geom& g, int64_t replicas, int target, L* lab, L* cnt,
-                       unsigned int* hist, unsigned long long* big, unsigned long long* nbig,
-                       int64_t big_cap, cudaStream_t s) {
-    const int64_t n = g.rows * g.Lx * replicas;
-    const int grid = grid_ccl(n);
-    cudaError_t e = cudaMemsetAsync(cnt, 0, sizeof(L) * (size_t)n, s);
+// Workspace sizes for launch_ccl (bytes), given the geometry and replicas.
+int64_t ccl_tiles(const Geom& g, int64_t replicas) {
+    const int64_t tx = (g.Lx + kTX - 1) / kTX, ty = (g.rows + kTR - 1) / kTR;
+    return tx * ty * replicas;
+}
+int64_t ccl_edge_entries(const Geom& g, int64_t replicas) { return ccl_tiles(g, replicas) * kEdge; }
+int64_t ccl_node_cap(const Geom& g, int64_t replicas) { return ccl_tiles(g, replicas) * kEdge; }
+
+// Fills hist ([replicas][kDense], zeroed by the caller) and the big list.
+// Workspace: edges (ccl_edge_entries uint32), node_size/node_par/node_rep
+// (node_cap uint32 each), root_size (node_cap uint64), counter (1 uint32).
+cudaError_t launch_ccl(const uint32_t* lat, const Geom& g, int64_t replicas, int target, uint32_t* edges,
+                       uint32_t* node_size, uint32_t* node_par, uint32_t* node_rep,
+                       unsigned long long* root_size, unsigned int* counter, unsigned int* hist,
+                       unsigned long long* big, unsigned long long* nbig, int64_t big_cap, cudaStream_t s) {
+    CclParams P{};
+    P.lat = lat;
+    P.g = g;
+    P.target = target;
+    P.tiles_x = (int)((g.Lx + kTX - 1) / kTX);
+    P.tiles_y = (int)((g.rows + kTR - 1) / kTR);
+    P.edges = edges;
+    P.node_size = node_size;
+    P.node_par = node_par;
+    P.node_rep = node_rep;
+    P.root_size = root_size;
+    P.node_count = counter;
+    P.hist = hist;
+    P.big = big;
+    P.nbig = nbig;
+    P.big_cap = big_cap;
+    P.node_cap = ccl_node_cap(g, replicas);
+    cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(unsigned int), s);
     if (e != cudaSuccess) return e;
-    ccl_init_kernel<L><<<grid, 256, 0, s>>>(lat, lab, g, replicas, target);
-    ccl_hook_kernel<L><<<grid, 256, 0, s>>>(lat, lab, g, replicas, target);
-    ccl_flatten_count_kernel<L><<<grid, 256, 0, s>>>(lab, cnt, g, replicas);
-    ccl_hist_kernel<L><<<grid, 256, 0, s>>>(lab, cnt, g, replicas, hist, big, nbig, big_cap);
-    for (int k = 0; k < 4; ++k) count_launch();
+    const int smem = 4 * (kTR * kTW + kSites / 2 + kSites / 32 + kSites) + 2 * kEdge;
+    e = cudaFuncSetAttribute(ccl_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    ccl_tile_kernel<<<dim3(P.tiles_x, P.tiles_y, (unsigned)replicas), kThreads, smem, s>>>(P);
+    count_launch();
+    const int64_t per_rep = (int64_t)P.tiles_x * P.tiles_y * (kTR + kTX);
+    int bx = grid_for_n(per_rep);
+    const int64_t cap = (148 * 16 + replicas - 1) / replicas;
+    if (bx > cap) bx = (int)(cap < 1 ? 1 : cap);
+    ccl_merge_kernel<<<dim3(bx, (unsigned)replicas), 256, 0, s>>>(P);
+    count_launch();
+    const int gn = grid_for_n(P.node_cap);
+    ccl_nodes_sum_kernel<<<gn, 256, 0, s>>>(P);
+    count_launch();
+    ccl_nodes_hist_rep_kernel<<<gn, 256, 0, s>>>(P, node_rep);
+    count_launch();
     return cudaGetLastError();
 }
-
-template cudaError_t launch_ccl<uint32_t>(const uint32_t*, const Geom&, int64_t, int, uint32_t*, uint32_t*,
-                                          unsigned int*, unsigned long long*, unsigned long long*, int64_t,
-                                          cudaStream_t);
-template cudaError_t launch_ccl<unsigned long long>(const uint32_t*, const Geom&, int64_t, int,
-                                                    unsigned long long*, unsigned long long*, unsigned int*,
-                                                    unsigned long long*, unsigned long long*, int64_t,
-                                                    cudaStream_t);
 
 }  // namespace kk

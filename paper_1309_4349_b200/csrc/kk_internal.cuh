@@ -59,6 +59,8 @@ struct Geom {
     int32_t pad;
 };
 
+__host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+
 __device__ __forceinline__ int64_t wrap_mod(int64_t v, int64_t L) {
     int64_t r = v % L;
     return r < 0 ? r + L : r;
@@ -119,6 +121,7 @@ struct PassParams {
     uint32_t sweep;
     int32_t j0;                // first iteration of this pass within the sweep
     uint32_t key0, key1;
+    uint32_t rk[20];           // Philox round keys: key0 + r*W0 (r<10), key1 + r*W1
     uint32_t thr[7];           // accept iff u32 <= thr[v+3] (R5)
 };
 

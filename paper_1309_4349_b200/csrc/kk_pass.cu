@@ -9,8 +9,11 @@
 // (32*TWI sites) of one replica and stages it in shared memory with HY = 3T
 // halo rows and one halo word per side (R8: after T iterations the
 // interior is exact).  The T iterations run entirely in shared memory; the
-// lattice crosses HBM once per T iterations (read tile+halo, write interior to
-// the other buffer).
+// lattice crosses HBM once per T iterations (read tile+halo, write the
+// interior to the other buffer).  Everything that depends only on the tile
+// position (global centre-pair indices per word, centre-row indices per row,
+// ownership masks) is tabulated in shared memory once per pass, so the inner
+// loop is pure 32-bit integer work.
 //
 // Work item = (row of the active class, 32-bit word): 8 centres.  The energy
 // change of all six possible exchanges of all 8 centres is computed with
@@ -18,7 +21,8 @@
 // the per-centre direction is selected with a 3-level bit-plane mux, and
 // acceptance is an integer compare against the precomputed threshold table
 // (north_star part 4; R5).  Flips are XOR masks applied with shared-memory
-// atomics (bits of different centres are disjoint, so the XORs commute).
+// atomics (bits of different centres are disjoint, so the XORs commute and
+// the result does not depend on thread scheduling).
 #include "kk_internal.cuh"
 
 namespace kk {
@@ -44,51 +48,82 @@ __device__ __forceinline__ uint32_t nib_view(uint32_t left, uint32_t mid, uint32
     return v & kNib;
 }
 
-struct ItemCtx {
-    uint32_t* tile;
-    int Wt;
-    uint32_t l;          // global centre row index (y >> 2)
-    uint32_t sweep, c3, key0, key1;
-    const uint32_t* thr; // shared-memory threshold table (7 entries)
-};
+// Four independent Philox4x32-10 streams, rounds interleaved for ILP; the
+// round keys come precomputed from the parameter bank (rk[0..9] for key
+// word 0, rk[10..19] for key word 1), so no per-item key schedule is issued.
+__device__ __forceinline__ void philox10_x4(const uint32_t m[4], uint32_t c1, uint32_t c2, uint32_t c3,
+                                            const uint32_t* rk, uint32_t out[4][4]) {
+    uint32_t a[4], b[4], c[4], d[4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+        a[p] = m[p];
+        b[p] = c1;
+        c[p] = c2;
+        d[p] = c3;
+    }
+#pragma unroll
+    for (int round = 0; round < 10; ++round) {
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            const uint64_t p0 = (uint64_t)kPhiloxM0 * a[p];
+            const uint64_t p1 = (uint64_t)kPhiloxM1 * c[p];
+            const uint32_t na = (uint32_t)(p1 >> 32) ^ b[p] ^ rk[round];
+            const uint32_t nc = (uint32_t)(p0 >> 32) ^ d[p] ^ rk[10 + round];
+            b[p] = (uint32_t)p1;
+            d[p] = (uint32_t)p0;
+            a[p] = na;
+            c[p] = nc;
+        }
+    }
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+        out[p][0] = a[p];
+        out[p][1] = b[p];
+        out[p][2] = c[p];
+        out[p][3] = d[p];
+    }
+}
 
 struct Acc {
     uint32_t attempted, trivial, accepted;
     int32_t dnab;
 };
 
-// One work item: the 8 centres of tile word (r, w).  m0 = global pair index of
-// the word's first centre pair; m_wrap = number of pairs per row (Lx/8) for
-// the (rare) word that straddles the x wrap; in_mask = nibble mask of centres
-// this CTA owns (stats), 0 for halo words.
+struct Tabs {
+    uint32_t* tile;            // H rows x WS words (col 0 and WS-1 are zero guards)
+    const uint4* mtab;         // [Wt] global pair indices of the word's 4 pairs
+    const uint32_t* wmask;     // [Wt] owned bits of the word (0 for halo words)
+    const uint32_t* rowl;      // [H] centre-row index l | owned-row flag << 31
+    const uint32_t* thr;       // [8] thresholds
+    int WS;
+};
+
+// One work item: the 8 centres of tile word w (column w+1) in row r.
 template <int KX>
-__device__ __forceinline__ void process_item(const ItemCtx& C, int r, int w, uint32_t m0,
-                                             uint32_t m_wrap, uint32_t in_mask, Acc& acc) {
-    // ---- random draws: 4 Philox calls, one per centre pair (R6)
+__device__ __forceinline__ void process_item(const Tabs& S, int r, int w, uint32_t sweep, uint32_t c3,
+                                             const uint32_t* rk, Acc& acc) {
+    const uint32_t rl = S.rowl[r];
+    const uint4 mq = S.mtab[w];
+    const uint32_t m[4] = {mq.x, mq.y, mq.z, mq.w};
+    uint32_t R4[4][4];
+    philox10_x4(m, rl & 0x7FFFFFFFu, sweep, c3, rk, R4);
     uint32_t u[8];
     uint32_t dv = 0;  // direction nibble vector: nibble q = direction of centre q
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
-        uint32_t m = m0 + p;
-        while (m >= m_wrap) m -= m_wrap;  // word straddling the x wrap (or Lx < 32)
-        const Words4 x = philox10(m, C.l, C.sweep, C.c3, C.key0, C.key1);
-        const uint32_t da = __umulhi(x.a, 6u);
-        const uint32_t db = __umulhi(x.c, 6u);
-        u[2 * p] = x.b;
-        u[2 * p + 1] = x.d;
-        dv |= (da << (8 * p)) | (db << (8 * p + 4));
+        dv |= (__umulhi(R4[p][0], 6u) << (8 * p)) | (__umulhi(R4[p][2], 6u) << (8 * p + 4));
+        u[2 * p] = R4[p][1];
+        u[2 * p + 1] = R4[p][3];
     }
 
-    // ---- neighbourhood: rows r-2..r+2, words w-1..w+1
-    const uint32_t* t = C.tile;
-    const int Wt = C.Wt;
+    // ---- neighbourhood: rows r-2..r+2, columns w..w+2 (w+1 is the word itself)
+    const uint32_t* t = S.tile + (r - 2) * S.WS + w;
     uint32_t L[5], M[5], R[5];
 #pragma unroll
     for (int k = 0; k < 5; ++k) {
-        const int base = (r - 2 + k) * Wt + w;
-        M[k] = t[base];
-        L[k] = (w > 0) ? t[base - 1] : 0u;
-        R[k] = (w + 1 < Wt) ? t[base + 1] : 0u;
+        L[k] = t[k * S.WS];
+        M[k] = t[k * S.WS + 1];
+        R[k] = t[k * S.WS + 2];
     }
 #define NV(dx, dy) nib_view<KX, dx>(L[(dy) + 2], M[(dy) + 2], R[(dy) + 2])
     const uint32_t c = NV(0, 0);
@@ -101,7 +136,7 @@ __device__ __forceinline__ void process_item(const ItemCtx& C, int r, int w, uin
     const uint32_t s_m2m1 = NV(-2, -1), s_m2m2 = NV(-2, -2), s_m1m2 = NV(-1, -2);
     const uint32_t s_0m2 = NV(0, -2);
 #undef NV
-    // e_i = S_c - S_t + 3 per nibble, S_c = A-count of the centre's exclusive
+    // e_i = S_c - S_t + 3 per nibble: S_c = A-count of the centre's exclusive
     // neighbours {d_{i+2}, d_{i+3}, d_{i+4}}, S_t = A-count of the partner's
     // {d_i+d_{i-1}, 2 d_i, d_i+d_{i+1}} (the two common neighbours cancel).
     constexpr uint32_t k3 = 0x33333333u;
@@ -135,88 +170,74 @@ __device__ __forceinline__ void process_item(const ItemCtx& C, int r, int w, uin
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
         const uint32_t iq = (idx >> (4 * q)) & 15u;
-        accb |= (u[q] <= C.thr[iq] ? 1u : 0u) << (4 * q);
+        accb |= (u[q] <= S.thr[iq] ? 1u : 0u) << (4 * q);
     }
     const uint32_t AN = accb & Dsel;
 
-    // ---- flips
-    if (AN) {
-        const uint32_t nb0 = ~b0 & kNib, nb1 = ~b1 & kNib, nb2 = ~b2 & kNib;
-        const uint32_t P0 = (AN & nb2 & nb1 & nb0) << KX;  // (+1, 0)
-        const uint32_t P1 = (AN & nb2 & nb1 & b0) << KX;   // (+1,+1)
-        const uint32_t P2 = (AN & nb2 & b1 & nb0) << KX;   // ( 0,+1)
-        const uint32_t P3 = (AN & nb2 & b1 & b0) << KX;    // (-1, 0)
-        const uint32_t P4 = (AN & b2 & nb1 & nb0) << KX;   // (-1,-1)
-        const uint32_t P5 = (AN & b2 & nb1 & b0) << KX;    // ( 0,-1)
-        const uint32_t Fr = (AN << KX) | (P0 << 1) | (P3 >> 1);
-        const uint32_t Fu = (P1 << 1) | P2;
-        const uint32_t Fd = (P4 >> 1) | P5;
-        uint32_t* row = C.tile + r * Wt + w;
-        atomicXor(row, Fr);
-        if (Fu) atomicXor(row + Wt, Fu);
-        if (Fd) atomicXor(row - Wt, Fd);
-        if constexpr (KX == 3) {  // centre at bit 31 moving right: partner in word w+1
-            if (w + 1 < Wt) {
-                if (P0 >> 31) atomicXor(row + 1, 1u);
-                if (P1 >> 31) atomicXor(row + Wt + 1, 1u);
-            }
-        }
-        if constexpr (KX == 0) {  // centre at bit 0 moving left: partner in word w-1
-            if (w > 0) {
-                if (P3 & 1u) atomicXor(row - 1, 0x80000000u);
-                if (P4 & 1u) atomicXor(row - Wt - 1, 0x80000000u);
-            }
-        }
+    // ---- flips (XOR masks; only words with changes are touched)
+    const uint32_t nb0 = ~b0 & kNib, nb1 = ~b1 & kNib, nb2 = ~b2 & kNib;
+    const uint32_t A0 = AN & nb2 & nb1;  // directions 0,1
+    const uint32_t A2 = AN & nb2 & b1;   // directions 2,3
+    const uint32_t A4 = AN & b2 & nb1;   // directions 4,5
+    const uint32_t P0 = (A0 & nb0) << KX;  // (+1, 0)
+    const uint32_t P1 = (A0 & b0) << KX;   // (+1,+1)
+    const uint32_t P2 = (A2 & nb0) << KX;  // ( 0,+1)
+    const uint32_t P3 = (A2 & b0) << KX;   // (-1, 0)
+    const uint32_t P4 = (A4 & nb0) << KX;  // (-1,-1)
+    const uint32_t P5 = (A4 & b0) << KX;   // ( 0,-1)
+    const uint32_t Fr = (AN << KX) | (P0 << 1) | (P3 >> 1);
+    const uint32_t Fu = (P1 << 1) | P2;
+    const uint32_t Fd = (P4 >> 1) | P5;
+    uint32_t* row = S.tile + r * S.WS + w + 1;
+    if (Fr) atomicXor(row, Fr);
+    if (Fu) atomicXor(row + S.WS, Fu);
+    if (Fd) atomicXor(row - S.WS, Fd);
+    if constexpr (KX == 3) {  // centre at bit 31 moving right: partner in the next word
+        if (P0 >> 31) atomicXor(row + 1, 1u);
+        if (P1 >> 31) atomicXor(row + S.WS + 1, 1u);
+    }
+    if constexpr (KX == 0) {  // centre at bit 0 moving left: partner in the previous word
+        if (P3 & 1u) atomicXor(row - 1, 0x80000000u);
+        if (P4 & 1u) atomicXor(row - S.WS - 1, 0x80000000u);
     }
 
     // ---- counters over owned centres
+    const uint32_t in_mask = (rl >> 31) ? ((S.wmask[w] >> KX) & kNib) : 0u;
     if (in_mask) {
         const uint32_t A = AN & in_mask;
         const uint32_t na = __popc(A);
         acc.attempted += __popc(in_mask);
         acc.trivial += __popc(in_mask & ~Dsel);
         acc.accepted += na;
-        const uint32_t S = idx & (A * 15u);
-        uint32_t s8 = (S & 0x0F0F0F0Fu) + ((S >> 4) & 0x0F0F0F0Fu);
+        const uint32_t Sg = idx & (A * 15u);
+        const uint32_t s8 = (Sg & 0x0F0F0F0Fu) + ((Sg >> 4) & 0x0F0F0F0Fu);
         const uint32_t sum = (s8 * 0x01010101u) >> 24;
         acc.dnab += 2 * ((int32_t)sum - 3 * (int32_t)na);
     }
 }
 
 template <int KX>
-__device__ __forceinline__ void run_iteration(const ItemCtx& Cbase, const PassParams& P, int64_t Y0,
-                                              int64_t X0, int HY, int H, int r_first, int nrows,
-                                              int64_t rows_interior_end, Acc& acc) {
-    const int Wt = Cbase.Wt;
+__device__ __forceinline__ void run_iteration(const Tabs& S, int Wt, int r_first, int nrows, uint32_t sweep,
+                                              uint32_t c3, const uint32_t* rk, Acc& acc) {
     const int items = nrows * Wt;
-    const int64_t Lx = P.g.Lx;
-    const uint32_t m_wrap = (uint32_t)(Lx >> 3);
+    // flattened (row, word) walk without per-item division
+    int a = threadIdx.x / Wt;
+    int w = threadIdx.x - a * Wt;
+    const int da = kThreads / Wt, dw = kThreads - da * Wt;
     for (int it = threadIdx.x; it < items; it += kThreads) {
-        const int a = it / Wt;
-        const int w = it - a * Wt;
-        const int r = r_first + 4 * a;
-        const int64_t y_local = Y0 - HY + r;
-        const int64_t yg = wrap_mod(P.g.y_begin + y_local, P.g.Ly);
-        ItemCtx C = Cbase;
-        C.l = (uint32_t)(yg >> 2);
-        const int64_t xu = X0 - 32 + 32 * (int64_t)w;  // unwrapped x of bit 0
-        const int64_t xg = wrap_mod(xu, Lx);
-        const uint32_t m0 = (uint32_t)(xg >> 3);
-        // owned centres: interior row, interior word, x < Lx
-        uint32_t in_mask = 0;
-        if (r >= HY && r < HY + P.THI && y_local < rows_interior_end && w >= 1 &&
-            w <= P.TWI && xu < Lx) {
-            const int64_t nbits = Lx - xu;
-            const uint32_t bits = nbits >= 32 ? 0xFFFFFFFFu : ((1u << nbits) - 1u);
-            in_mask = (bits >> KX) & kNib;
+        process_item<KX>(S, r_first + 4 * a, w, sweep, c3, rk, acc);
+        a += da;
+        w += dw;
+        if (w >= Wt) {
+            w -= Wt;
+            ++a;
         }
-        process_item<KX>(C, r, w, m0, m_wrap, in_mask, acc);
     }
 }
 
 template <int T>
-__global__ void __launch_bounds__(kThreads) pass_kernel(const PassParams P) {
-    extern __shared__ uint32_t tile[];
+__global__ void __launch_bounds__(kThreads, 4) pass_kernel(const PassParams P) {
+    extern __shared__ uint32_t smem[];
     __shared__ uint32_t thr[8];
     __shared__ unsigned long long red[4][kThreads / 32];
     constexpr int HY = 3 * T;
@@ -225,12 +246,40 @@ __global__ void __launch_bounds__(kThreads) pass_kernel(const PassParams P) {
     const int64_t Y0 = (int64_t)band * P.THI;
     const int64_t X0 = (int64_t)blockIdx.x * P.TWI * 32;
     const int Wt = P.TWI + 2;
+    const int WS = Wt + 2;
     const int H = P.THI + 2 * HY;
     const Geom& g = P.g;
     const uint32_t* src = P.src + rep * g.rep_words;
     const uint32_t* htop = P.halo_top ? P.halo_top + rep * P.halo_rep_words : nullptr;
     const uint32_t* hbot = P.halo_bot ? P.halo_bot + rep * P.halo_rep_words : nullptr;
+
+    uint32_t* tile = smem;                                        // [H][WS]
+    uint4* mtab = reinterpret_cast<uint4*>(tile + ((H * WS + 3) & ~3));  // [Wt], 16-byte aligned
+    uint32_t* wmask = reinterpret_cast<uint32_t*>(mtab + Wt);     // [Wt]
+    uint32_t* rowl = wmask + Wt;                                  // [H]
     if (threadIdx.x < 7) thr[threadIdx.x] = P.thr[threadIdx.x];
+
+    // ---- per-pass tables
+    const int64_t m_wrap = g.Lx >> 3;
+    for (int w = threadIdx.x; w < Wt; w += kThreads) {
+        const int64_t xu = X0 - 32 + 32 * (int64_t)w;  // unwrapped x of bit 0
+        const int64_t xg = wrap_mod(xu, g.Lx);
+        uint32_t mm[4];
+        for (int p = 0; p < 4; ++p) mm[p] = (uint32_t)(((xg >> 3) + p) % m_wrap);
+        mtab[w] = make_uint4(mm[0], mm[1], mm[2], mm[3]);
+        uint32_t own = 0;
+        if (w >= 1 && w <= P.TWI && xu < g.Lx) {
+            const int64_t nbits = g.Lx - xu;
+            own = nbits >= 32 ? 0xFFFFFFFFu : ((1u << nbits) - 1u);
+        }
+        wmask[w] = own;
+    }
+    for (int r = threadIdx.x; r < H; r += kThreads) {
+        const int64_t y_local = Y0 - HY + r;
+        const int64_t yg = wrap_mod(g.y_begin + y_local, g.Ly);
+        const bool owned = r >= HY && r < HY + P.THI && y_local < g.rows;
+        rowl[r] = (uint32_t)(yg >> 2) | (owned ? 0x80000000u : 0u);
+    }
 
     // ---- stage tile + halo (coalesced 32-bit loads, periodic in x)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -238,6 +287,11 @@ __global__ void __launch_bounds__(kThreads) pass_kernel(const PassParams P) {
     const int64_t gw0 = X0 / 32 - 1;
     for (int r = warp; r < H; r += kThreads / 32) {
         const uint32_t* row = row_source(g, src, htop, hbot, HY, Y0 - HY + r);
+        uint32_t* trow = tile + r * WS;
+        if (lane == 0) {
+            trow[0] = 0u;
+            trow[WS - 1] = 0u;
+        }
         for (int w = lane; w < Wt; w += 32) {
             uint32_t v = 0;
             if (row) {
@@ -253,41 +307,40 @@ __global__ void __launch_bounds__(kThreads) pass_kernel(const PassParams P) {
                     v = get32(row, p, g);
                 }
             }
-            tile[r * Wt + w] = v;
+            trow[w + 1] = v;
         }
     }
     __syncthreads();
 
     const Words4 sched = philox10(0u, 0u, P.sweep, ((uint32_t)rep << 8) | kTagSchedule, P.key0, P.key1);
     Acc acc = {0u, 0u, 0u, 0};
-    ItemCtx C;
-    C.tile = tile;
-    C.Wt = Wt;
-    C.l = 0;
-    C.sweep = P.sweep;
-    C.key0 = P.key0;
-    C.key1 = P.key1;
-    C.thr = thr;
-    const int64_t rows_interior_end = g.rows;  // local rows beyond the slab are never owned
+    Tabs S;
+    S.tile = tile;
+    S.mtab = mtab;
+    S.wmask = wmask;
+    S.rowl = rowl;
+    S.thr = thr;
+    S.WS = WS;
+    const int phase0 = (int)((Y0 - HY + g.y_begin) & 3);
 
 #pragma unroll 1
     for (int t = 0; t < T; ++t) {
         const int j = P.j0 + t;
         const uint32_t k = ((j < 8 ? sched.a : sched.b) >> (4 * (j & 7))) & 15u;
         const int kx = (int)(k & 3u), ky = (int)(k >> 2);
-        C.c3 = ((uint32_t)rep << 8) | (uint32_t)j;
+        const uint32_t c3 = ((uint32_t)rep << 8) | (uint32_t)j;
         // rows whose centres can still influence the interior (light cone)
         const int ext = 3 * (T - 1 - t) + 1;
         const int r_lo = max(2, HY - ext);
         const int r_hi = min(H - 2, HY + P.THI + ext);
-        const int phase = (int)((ky - ((Y0 - HY + g.y_begin) & 3)) & 3);  // r = phase (mod 4)
+        const int phase = (ky - phase0) & 3;  // active rows: r = phase (mod 4)
         const int r_first = r_lo + ((phase - r_lo) & 3);
         const int nrows = r_hi > r_first ? (r_hi - r_first + 3) / 4 : 0;
         switch (kx) {
-            case 0: run_iteration<0>(C, P, Y0, X0, HY, H, r_first, nrows, rows_interior_end, acc); break;
-            case 1: run_iteration<1>(C, P, Y0, X0, HY, H, r_first, nrows, rows_interior_end, acc); break;
-            case 2: run_iteration<2>(C, P, Y0, X0, HY, H, r_first, nrows, rows_interior_end, acc); break;
-            default: run_iteration<3>(C, P, Y0, X0, HY, H, r_first, nrows, rows_interior_end, acc); break;
+            case 0: run_iteration<0>(S, Wt, r_first, nrows, P.sweep, c3, P.rk, acc); break;
+            case 1: run_iteration<1>(S, Wt, r_first, nrows, P.sweep, c3, P.rk, acc); break;
+            case 2: run_iteration<2>(S, Wt, r_first, nrows, P.sweep, c3, P.rk, acc); break;
+            default: run_iteration<3>(S, Wt, r_first, nrows, P.sweep, c3, P.rk, acc); break;
         }
         __syncthreads();
     }
@@ -300,7 +353,7 @@ __global__ void __launch_bounds__(kThreads) pass_kernel(const PassParams P) {
         for (int w = 1 + lane; w <= P.TWI; w += 32) {
             const int64_t gw = X0 / 32 + (w - 1);
             if (gw >= g.W) break;
-            dst[y * g.W + gw] = tile[r * Wt + w] & word_mask(g, gw);
+            dst[y * g.W + gw] = tile[r * WS + w + 1] & word_mask(g, gw);
         }
     }
 
@@ -330,18 +383,23 @@ __global__ void __launch_bounds__(kThreads) pass_kernel(const PassParams P) {
 
 }  // namespace
 
-int pass_smem_bytes(int T, int THI, int TWI) { return (THI + 6 * T) * (TWI + 2) * 4; }
+int pass_smem_bytes(int T, int THI, int TWI) {
+    const int H = THI + 6 * T, Wt = TWI + 2, WS = Wt + 2;
+    int tile_bytes = H * WS * 4;
+    tile_bytes = (tile_bytes + 15) / 16 * 16;
+    return tile_bytes + Wt * 16 + Wt * 4 + H * 4;
+}
 
 cudaError_t launch_pass(int T, const PassParams& P, int grid_y, int replicas, cudaStream_t stream) {
     const int smem = pass_smem_bytes(T, P.THI, P.TWI);
     dim3 grid(P.tiles_x, grid_y, replicas);
     if (grid_y == 0) return cudaSuccess;
     cudaError_t e = cudaSuccess;
-#define KK_LAUNCH(TT)                                                                      \
-    case TT:                                                                               \
+#define KK_LAUNCH(TT)                                                                                  \
+    case TT:                                                                                           \
         e = cudaFuncSetAttribute(pass_kernel<TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
-        if (e != cudaSuccess) return e;                                                    \
-        pass_kernel<TT><<<grid, kThreads, smem, stream>>>(P);                              \
+        if (e != cudaSuccess) return e;                                                                \
+        pass_kernel<TT><<<grid, kThreads, smem, stream>>>(P);                                          \
         break;
     switch (T) {
         KK_LAUNCH(1)

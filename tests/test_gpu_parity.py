@@ -233,3 +233,24 @@ def test_bench_lattice_65536_window_and_invariants():
         exp = win[hy:hy + H]
         got = inputs.unpack_rows(after[[(y0 + r) % Ly for r in range(H)]], Lx)
         assert np.array_equal(got, exp)
+
+
+def test_cluster_histogram_random_stress():
+    """Random lattices over many shapes (several CCL tiles, ragged edges,
+    replicas): the multiset must equal the oracle's every time (this caught a
+    flatten-phase race in the tile kernel)."""
+    from paper_1309_4349_b200 import kk
+    rng = np.random.default_rng(11)
+    for trial in range(40):
+        Lx = int(rng.choice([8, 40, 256, 264, 400, 520, 1024]))
+        Ly = int(rng.choice([4, 32, 36, 64, 100, 400]))
+        R = int(rng.choice([1, 2, 3]))
+        f = float(rng.choice([0.3, 0.5, 0.6, 0.7]))
+        lat = inputs.random_lattice(Lx, Ly, f, seed=trial, replicas=R)
+        L = _lat(Lx, Ly, 0.5, 0.5, 1, replicas=R, init=kk.KK_INIT_EMPTY)
+        L.set_lattice(lat)
+        for target in (0, 1):
+            got = L.cluster_histogram(target)
+            for r in range(R):
+                assert got[r] == O.cluster_histogram(lat[r], target), (Lx, Ly, R, r, f, target)
+        L.close()
