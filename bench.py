@@ -50,7 +50,7 @@ def parse():
     p.add_argument("--omega", type=float, default=0.6)
     p.add_argument("--fraction", type=float, default=0.5)
     p.add_argument("--seed", type=int, default=20261018)
-    p.add_argument("--T", type=int, default=4, help="MPKK iterations per HBM pass")
+    p.add_argument("--T", type=int, default=8, help="MPKK iterations per HBM pass")
     p.add_argument("--no-ccl", action="store_true", help="skip the cluster histogram in the step")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")

@@ -108,13 +108,28 @@ __device__ __forceinline__ void hist_add(const CclParams& P, int64_t rep, unsign
 }
 
 // ---- phase 1: one CTA per tile ------------------------------------------------
+// Row runs: along a row, consecutive target sites are connected by the (+1,0)
+// bond, so each maximal run is labelled by its first site without any union.
+// Union-find then only links runs of neighbouring rows, once per overlapping
+// run pair and bond type ((0,+1) and (+1,+1)): a union point is placed where
+// the overlap starts, i.e. at a run start of either row.
+
+// First site (tile index) of the run containing target site x of row r.
+__device__ __forceinline__ uint32_t run_start(const uint32_t* S, int r, int x) {
+    int wi = x >> 5;
+    uint32_t m = S[r * kTW + wi] & (0xFFFFFFFFu >> (31 - (x & 31)));
+    while (m == 0) m = S[r * kTW + (--wi)];
+    return (uint32_t)(r * kTX + 32 * wi + 31 - __clz(m));
+}
+
 __global__ void __launch_bounds__(kThreads) ccl_tile_kernel(const CclParams P) {
     extern __shared__ uint32_t smem[];
-    uint32_t* bits = smem;                                            // [kTR*kTW]
-    uint32_t* cnt = bits + kTR * kTW;                                 // [kSites/2] two 16-bit counters/word
-    uint32_t* touch = cnt + kSites / 2;                               // [kSites/32] edge-touch flag per root
-    uint32_t* lab = touch + kSites / 32;                              // [kSites]
-    uint16_t* node_s = reinterpret_cast<uint16_t*>(lab + kSites);     // [kEdge] sizes of edge nodes
+    uint32_t* tb = smem;                 // [kTR*kTW] target bits
+    uint32_t* S = tb + kTR * kTW;        // [kTR*kTW] run-start bits
+    uint32_t* touch = S + kTR * kTW;     // [kSites/32] edge-touch flag per root
+    uint32_t* lab = touch + kSites / 32; // [kSites] parent of each run start
+    uint32_t* cnt = lab + kSites;        // [kSites] size per root, then local node index
+    uint16_t* node_s = reinterpret_cast<uint16_t*>(cnt + kSites);  // [kEdge]
     __shared__ unsigned int n_nodes, node_base;
 
     const Geom& g = P.g;
@@ -131,54 +146,78 @@ __global__ void __launch_bounds__(kThreads) ccl_tile_kernel(const CclParams P) {
         const int r = i / kTW, w = i - r * kTW;
         uint32_t v = 0;
         if (r < h_tile && 32 * w < w_tile) {
-            const int64_t gw = X0 / 32 + w;
-            v = (lat[(Y0 + r) * g.W + gw] ^ tmask);         // 1 = target site
+            v = lat[(Y0 + r) * g.W + X0 / 32 + w] ^ tmask;   // 1 = target site
             const int nv = w_tile - 32 * w;
             if (nv < 32) v &= (1u << nv) - 1u;
         }
-        bits[i] = v;
+        tb[i] = v;
     }
-    for (int i = threadIdx.x; i < kSites / 2; i += kThreads) cnt[i] = 0;
     for (int i = threadIdx.x; i < kSites / 32; i += kThreads) touch[i] = 0;
     __syncthreads();
-    for (int i = threadIdx.x; i < kSites; i += kThreads) {
-        const bool t = (bits[i >> 5] >> (i & 31)) & 1u;
-        lab[i] = t ? (uint32_t)i : kNone;
-    }
-    __syncthreads();
-    // unions over in-tile bonds (+1,0) (0,+1) (+1,+1)
-    for (int i = threadIdx.x; i < kSites; i += kThreads) {
-        if (!((bits[i >> 5] >> (i & 31)) & 1u)) continue;
-        const int r = i / kTX, x = i - r * kTX;
-        if (x + 1 < w_tile && ((bits[(i + 1) >> 5] >> ((i + 1) & 31)) & 1u)) union32(lab, i, i + 1);
-        if (r + 1 < h_tile) {
-            const int j = i + kTX;
-            if ((bits[j >> 5] >> (j & 31)) & 1u) union32(lab, i, j);
-            if (x + 1 < w_tile && ((bits[(j + 1) >> 5] >> ((j + 1) & 31)) & 1u)) union32(lab, i, j + 1);
+    for (int i = threadIdx.x; i < kTR * kTW; i += kThreads) {
+        const int w = i % kTW;
+        const uint32_t prev = w ? (tb[i - 1] >> 31) : 0u;
+        const uint32_t st = tb[i] & ~((tb[i] << 1) | prev);
+        S[i] = st;
+        const int base = (i / kTW) * kTX + 32 * w;
+        for (uint32_t m = st; m; m &= m - 1) {
+            const int b = __ffs(m) - 1;
+            lab[base + b] = base + b;
+            cnt[base + b] = 0;
         }
     }
     __syncthreads();
-    // flatten, count, mark edge-touching roots
-    for (int i = threadIdx.x; i < kSites; i += kThreads) {
-        if (lab[i] == kNone) continue;
-        const uint32_t root = root_of(lab, (uint32_t)i);
-        lab[i] = root;
-        atomicAdd(&cnt[root >> 1], 1u << (16 * (root & 1)));
-        const int r = i / kTX, x = i - r * kTX;
-        if (r == 0 || r == h_tile - 1 || x == 0 || x == w_tile - 1) atomicOr(&touch[root >> 5], 1u << (root & 31));
+    // unions between runs of rows r and r+1
+    for (int i = threadIdx.x; i < kTR * kTW; i += kThreads) {
+        const int r = i / kTW, w = i - r * kTW;
+        if (r + 1 >= h_tile) continue;
+        const uint32_t t0 = tb[i], t1 = tb[i + kTW], S0 = S[i], S1 = S[i + kTW];
+        const uint32_t t1n = (w + 1 < kTW) ? tb[i + kTW + 1] : 0u;
+        const uint32_t S1n = (w + 1 < kTW) ? S[i + kTW + 1] : 0u;
+        const uint32_t t1s = (t1 >> 1) | (t1n << 31);   // bit x <- site x+1 of row r+1
+        const uint32_t S1s = (S1 >> 1) | (S1n << 31);
+        const uint32_t V1 = t0 & t1 & (S0 | S1);        // (0,+1) union points
+        const uint32_t V2 = t0 & t1s & (S0 | S1s);      // (+1,+1) union points
+        for (uint32_t m = V1; m; m &= m - 1) {
+            const int x = 32 * w + __ffs(m) - 1;
+            union32(lab, run_start(S, r, x), run_start(S, r + 1, x));
+        }
+        for (uint32_t m = V2; m; m &= m - 1) {
+            const int x = 32 * w + __ffs(m) - 1;
+            union32(lab, run_start(S, r, x), run_start(S, r + 1, x + 1));
+        }
+    }
+    __syncthreads();
+    // sizes per root (one atomic per run segment) and edge-touch flags
+    for (int i = threadIdx.x; i < kTR * kTW; i += kThreads) {
+        const int r = i / kTW, w = i - r * kTW;
+        const bool edge_row = (r == 0 || r == h_tile - 1);
+        for (uint32_t m = tb[i]; m;) {
+            const uint64_t M = m, Lb = M & (~M + 1);
+            const uint32_t seg = (uint32_t)(((M + Lb) ^ M) & M);
+            m &= ~seg;
+            const int x0 = 32 * w + __ffs(seg) - 1;
+            const int x1 = 32 * w + 31 - __clz(seg);
+            const uint32_t root = root_of(lab, run_start(S, r, x0));
+            atomicAdd(&cnt[root], (uint32_t)__popc(seg));
+            if (edge_row || x0 == 0 || x1 == w_tile - 1) atomicOr(&touch[root >> 5], 1u << (root & 31));
+        }
     }
     __syncthreads();
     // complete components -> histogram; edge components -> local node index
-    uint16_t* cnt16 = reinterpret_cast<uint16_t*>(cnt);
-    for (int i = threadIdx.x; i < kSites; i += kThreads) {
-        if (lab[i] != (uint32_t)i) continue;
-        const uint32_t s = cnt16[i];
-        if ((touch[i >> 5] >> (i & 31)) & 1u) {
-            const unsigned int k = atomicAdd(&n_nodes, 1u);
-            node_s[k] = (uint16_t)s;
-            cnt16[i] = (uint16_t)k;   // root -> local node index (this thread owns this half)
-        } else {
-            hist_add(P, rep, s);
+    for (int i = threadIdx.x; i < kTR * kTW; i += kThreads) {
+        const int base = (i / kTW) * kTX + 32 * (i % kTW);
+        for (uint32_t m = S[i]; m; m &= m - 1) {
+            const uint32_t s0 = base + __ffs(m) - 1;
+            if (lab[s0] != s0) continue;
+            const uint32_t sz = cnt[s0];
+            if ((touch[s0 >> 5] >> (s0 & 31)) & 1u) {
+                const unsigned int k = atomicAdd(&n_nodes, 1u);
+                node_s[k] = (uint16_t)sz;
+                cnt[s0] = k;   // root -> local node index
+            } else {
+                hist_add(P, rep, sz);
+            }
         }
     }
     __syncthreads();
@@ -196,17 +235,15 @@ __global__ void __launch_bounds__(kThreads) ccl_tile_kernel(const CclParams P) {
     // edge export
     const int64_t tile = (rep * P.tiles_y + ty) * P.tiles_x + tx;
     uint32_t* E = P.edges + tile * kEdge;
-    auto node_of = [&](int r, int x) -> uint32_t {
-        if (r >= h_tile || x >= w_tile) return kNone;
-        const uint32_t l = lab[r * kTX + x];
-        return l == kNone ? kNone : base + cnt16[l];
-    };
     for (int e = threadIdx.x; e < kEdge; e += kThreads) {
-        uint32_t v;
-        if (e < kTX) v = node_of(0, e);                                   // top row
-        else if (e < 2 * kTX) v = node_of(h_tile - 1, e - kTX);           // bottom row
-        else if (e < 2 * kTX + kTR) v = node_of(e - 2 * kTX, 0);          // left column
-        else v = node_of(e - 2 * kTX - kTR, w_tile - 1);                  // right column
+        int r, x;
+        if (e < kTX) { r = 0; x = e; }                                   // top row
+        else if (e < 2 * kTX) { r = h_tile - 1; x = e - kTX; }           // bottom row
+        else if (e < 2 * kTX + kTR) { r = e - 2 * kTX; x = 0; }          // left column
+        else { r = e - 2 * kTX - kTR; x = w_tile - 1; }                  // right column
+        uint32_t v = kNone;
+        if (r < h_tile && x < w_tile && ((tb[r * kTW + (x >> 5)] >> (x & 31)) & 1u))
+            v = base + cnt[root_of(lab, run_start(S, r, x))];
         E[e] = v;
     }
 }
@@ -313,7 +350,7 @@ cudaError_t launch_ccl(const uint32_t* lat, const Geom& g, int64_t replicas, int
     P.node_cap = ccl_node_cap(g, replicas);
     cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(unsigned int), s);
     if (e != cudaSuccess) return e;
-    const int smem = 4 * (kTR * kTW + kSites / 2 + kSites / 32 + kSites) + 2 * kEdge;
+    const int smem = 4 * (2 * kTR * kTW + kSites / 32 + 2 * kSites) + 2 * kEdge;
     e = cudaFuncSetAttribute(ccl_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     ccl_tile_kernel<<<dim3(P.tiles_x, P.tiles_y, (unsigned)replicas), kThreads, smem, s>>>(P);

@@ -206,7 +206,7 @@ def test_bench_lattice_65536_window_and_invariants():
     invariants over the whole lattice + sampled window parity for one pass."""
     from paper_1309_4349_b200 import kk
     Lx = Ly = 65536
-    L = _lat(Lx, Ly, 0.5, 0.6, 99, init=kk.KK_INIT_BLOCK)
+    L = _lat(Lx, Ly, 0.5, 0.6, 99, init=kk.KK_INIT_BLOCK, iters_per_pass=4)
     nA = L.composition()[0]
     assert nA == Lx * Ly // 2
     L.sweep(1)                                    # mix the block start
