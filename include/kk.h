@@ -119,6 +119,29 @@ int kk_stats(kk_handle h, int64_t* out, int reset, void* stream);
 int kk_cluster_histogram(kk_handle h, int target, int64_t* out, int64_t capacity,
                          int64_t* n_out, void* stream);
 
+/* Cluster histogram of a row slab (multi-GPU, R9): clusters are labelled with
+ * NO bonds across the slab's first/last rows.  Clusters touching neither row
+ * are complete: rows (size, count) go to hist_out (host, 2*capacity int64).
+ * Clusters touching them are "open": their sizes go to open_sizes (device,
+ * open_cap uint64) under compact ids 0..n_open-1, and top_ids/bot_ids (device,
+ * Lx uint32 each) give the open id of every site of the first/last row
+ * (0xFFFFFFFF = not a target site).  One replica per handle.  Works on full
+ * lattices too (then the wrap bond rows are treated as open). */
+int kk_cluster_slab(kk_handle h, int target, int64_t* hist_out, int64_t capacity, int64_t* n_hist,
+                    uint32_t* top_ids, uint32_t* bot_ids, unsigned long long* open_sizes, int64_t open_cap,
+                    int64_t* n_open, void* stream);
+
+/* Join the open clusters of nslabs consecutive slabs (slab s's last row
+ * bonds to slab (s+1) % nslabs's first row with (0,+1) and (+1,+1)).  Inputs on
+ * the current device: top_ids/bot_ids [nslabs][Lx] as returned by
+ * kk_cluster_slab (per-slab open ids), sizes [n_nodes] = every slab's
+ * open_sizes concatenated; slab_offsets (host, nslabs int64) = index of each
+ * slab's first open cluster in `sizes`.  Output rows (size, count) of the
+ * merged clusters (host, 2*capacity int64). */
+int kk_cluster_join(int64_t Lx, int64_t nslabs, const uint32_t* top_ids, const uint32_t* bot_ids,
+                    const int64_t* slab_offsets, const unsigned long long* sizes, int64_t n_nodes,
+                    int64_t* hist_out, int64_t capacity, int64_t* n_hist, void* stream);
+
 /* Lattice transfer.  Byte form: host uint8[replicas][y_count][Lx], 1 = A.
  * Packed form: host uint32[replicas][y_count][W] in the device layout.  The
  * packed form is what end-to-end callers use (1 bit per site). */

@@ -38,7 +38,11 @@ int64_t ccl_node_cap(const Geom& g, int64_t replicas);
 cudaError_t launch_ccl(const uint32_t* lat, const Geom& g, int64_t replicas, int target, uint32_t* edges,
                        uint32_t* node_size, uint32_t* node_par, uint32_t* node_rep,
                        unsigned long long* root_size, unsigned int* counter, unsigned int* hist,
-                       unsigned long long* big, unsigned long long* nbig, int64_t big_cap, cudaStream_t s);
+                       unsigned long long* big, unsigned long long* nbig, int64_t big_cap, cudaStream_t s,
+                       const SlabCclArgs* slab);
+cudaError_t launch_join(int64_t Lx, int64_t nslabs, const uint32_t* top, const uint32_t* bot, const uint32_t* off,
+                        const unsigned long long* sizes, int64_t n, uint32_t* par, unsigned long long* rsize,
+                        unsigned long long* out, unsigned int* nout, cudaStream_t s);
 
 }  // namespace kk
 
@@ -66,6 +70,9 @@ struct kk_lattice {
     uint32_t* node_rep = nullptr;
     unsigned long long* root_size = nullptr;
     unsigned int* counter = nullptr;
+    uint32_t* open_flag = nullptr;
+    uint32_t* compact = nullptr;
+    unsigned int* open_count = nullptr;
     unsigned int* hist = nullptr;
     unsigned long long* big = nullptr;
     unsigned long long* nbig = nullptr;
@@ -194,6 +201,9 @@ void free_all(kk_lattice* h) {
     cudaFree(h->node_rep);
     cudaFree(h->root_size);
     cudaFree(h->counter);
+    cudaFree(h->open_flag);
+    cudaFree(h->compact);
+    cudaFree(h->open_count);
     cudaFree(h->hist);
     cudaFree(h->big);
     cudaFree(h->nbig);
@@ -529,29 +539,30 @@ int kk_stats(kk_handle h, int64_t* out, int reset, void* stream) {
     return KK_OK;
 }
 
-int kk_cluster_histogram(kk_handle h, int target, int64_t* out, int64_t capacity, int64_t* n_out, void* stream) {
-    KK_CHECK_HANDLE(h);
-    if (!n_out) return fail(KK_ERR_ARG, "n_out is null");
-    if (!h->g.periodic) return fail(KK_ERR_STATE, "cluster histogram needs a full-lattice handle");
-    cudaStream_t s = S(stream);
+}  // extern "C"
+
+namespace {
+
+int ensure_ccl_workspace(kk_lattice* h) {
+    if (h->edges) return KK_OK;
     const int64_t n = h->g.Lx * h->g.rows * h->R;
-    if (!h->edges) {
-        const int64_t ne = ccl_edge_entries(h->g, h->R), nn = ccl_node_cap(h->g, h->R);
-        h->big_cap = n / kDense + 16;
-        if (cudaMalloc(&h->edges, 4 * ne) || cudaMalloc(&h->node_size, 4 * nn) ||
-            cudaMalloc(&h->node_par, 4 * nn) || cudaMalloc(&h->node_rep, 4 * nn) ||
-            cudaMalloc(&h->root_size, 8 * nn) || cudaMalloc(&h->counter, sizeof(unsigned int)) ||
-            cudaMalloc(&h->hist, sizeof(unsigned int) * kDense * h->R) ||
-            cudaMalloc(&h->big, sizeof(unsigned long long) * 2 * h->big_cap) ||
-            cudaMalloc(&h->nbig, sizeof(unsigned long long))) {
-            cudaGetLastError();
-            return fail(KK_ERR_NOMEM, "cluster workspace: device allocation failed");
-        }
+    const int64_t ne = ccl_edge_entries(h->g, h->R), nn = ccl_node_cap(h->g, h->R);
+    h->big_cap = n / kDense + 16;
+    if (cudaMalloc(&h->edges, 4 * ne) || cudaMalloc(&h->node_size, 4 * nn) || cudaMalloc(&h->node_par, 4 * nn) ||
+        cudaMalloc(&h->node_rep, 4 * nn) || cudaMalloc(&h->root_size, 8 * nn) ||
+        cudaMalloc(&h->counter, sizeof(unsigned int)) || cudaMalloc(&h->open_flag, 4 * nn) ||
+        cudaMalloc(&h->compact, 4 * nn) || cudaMalloc(&h->open_count, sizeof(unsigned int)) ||
+        cudaMalloc(&h->hist, sizeof(unsigned int) * kDense * h->R) ||
+        cudaMalloc(&h->big, sizeof(unsigned long long) * 2 * h->big_cap) ||
+        cudaMalloc(&h->nbig, sizeof(unsigned long long))) {
+        cudaGetLastError();
+        return fail(KK_ERR_NOMEM, "cluster workspace: device allocation failed");
     }
-    KK_CUDA(cudaMemsetAsync(h->hist, 0, sizeof(unsigned int) * kDense * h->R, s));
-    KK_CUDA(cudaMemsetAsync(h->nbig, 0, sizeof(unsigned long long), s));
-    KK_CUDA(launch_ccl(h->buf[h->cur], h->g, h->R, target, h->edges, h->node_size, h->node_par, h->node_rep,
-                       h->root_size, h->counter, h->hist, h->big, h->nbig, h->big_cap, s));
+    return KK_OK;
+}
+
+// Dense histogram + big list -> rows (replica, size, count) sorted.
+int collect_hist_rows(kk_lattice* h, cudaStream_t s, std::vector<int64_t>& rows) {
     std::vector<unsigned int> hist((size_t)kDense * h->R);
     unsigned long long nb = 0;
     KK_CUDA(cudaMemcpyAsync(hist.data(), h->hist, sizeof(unsigned int) * kDense * h->R, cudaMemcpyDeviceToHost, s));
@@ -566,7 +577,7 @@ int kk_cluster_histogram(kk_handle h, int target, int64_t* out, int64_t capacity
     std::vector<std::pair<int64_t, int64_t>> bigl(nb);
     for (unsigned long long k = 0; k < nb; ++k) bigl[k] = {(int64_t)big[2 * k], (int64_t)big[2 * k + 1]};
     std::sort(bigl.begin(), bigl.end());
-    std::vector<int64_t> rows;
+    rows.clear();
     size_t bi = 0;
     for (int64_t r = 0; r < h->R; ++r) {
         for (int sz = 1; sz < kDense; ++sz) {
@@ -580,10 +591,108 @@ int kk_cluster_histogram(kk_handle h, int target, int64_t* out, int64_t capacity
             rows.push_back(r); rows.push_back(sz); rows.push_back(c);
         }
     }
+    return KK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int kk_cluster_histogram(kk_handle h, int target, int64_t* out, int64_t capacity, int64_t* n_out, void* stream) {
+    KK_CHECK_HANDLE(h);
+    if (!n_out) return fail(KK_ERR_ARG, "n_out is null");
+    if (!h->g.periodic) return fail(KK_ERR_STATE, "cluster histogram needs a full-lattice handle (kk_cluster_slab)");
+    cudaStream_t s = S(stream);
+    int rc = ensure_ccl_workspace(h);
+    if (rc != KK_OK) return rc;
+    KK_CUDA(cudaMemsetAsync(h->hist, 0, sizeof(unsigned int) * kDense * h->R, s));
+    KK_CUDA(cudaMemsetAsync(h->nbig, 0, sizeof(unsigned long long), s));
+    KK_CUDA(launch_ccl(h->buf[h->cur], h->g, h->R, target, h->edges, h->node_size, h->node_par, h->node_rep,
+                       h->root_size, h->counter, h->hist, h->big, h->nbig, h->big_cap, s, nullptr));
+    std::vector<int64_t> rows;
+    rc = collect_hist_rows(h, s, rows);
+    if (rc != KK_OK) return rc;
     const int64_t nrows = (int64_t)rows.size() / 3;
     *n_out = nrows;
     if (nrows > capacity || (!out && nrows > 0)) return fail(KK_ERR_CAPACITY, "histogram buffer too small");
     if (nrows) std::memcpy(out, rows.data(), sizeof(int64_t) * rows.size());
+    return KK_OK;
+}
+
+int kk_cluster_slab(kk_handle h, int target, int64_t* hist_out, int64_t capacity, int64_t* n_hist,
+                    uint32_t* top_ids, uint32_t* bot_ids, unsigned long long* open_sizes, int64_t open_cap,
+                    int64_t* n_open, void* stream) {
+    KK_CHECK_HANDLE(h);
+    if (!n_hist || !n_open || !top_ids || !bot_ids || !open_sizes) return fail(KK_ERR_ARG, "null argument");
+    if (h->R != 1) return fail(KK_ERR_STATE, "kk_cluster_slab: one replica per handle");
+    cudaStream_t s = S(stream);
+    int rc = ensure_ccl_workspace(h);
+    if (rc != KK_OK) return rc;
+    KK_CUDA(cudaMemsetAsync(h->hist, 0, sizeof(unsigned int) * kDense, s));
+    KK_CUDA(cudaMemsetAsync(h->nbig, 0, sizeof(unsigned long long), s));
+    SlabCclArgs a{h->open_flag, h->compact, open_sizes, h->open_count, open_cap, top_ids, bot_ids};
+    KK_CUDA(launch_ccl(h->buf[h->cur], h->g, 1, target, h->edges, h->node_size, h->node_par, h->node_rep,
+                       h->root_size, h->counter, h->hist, h->big, h->nbig, h->big_cap, s, &a));
+    unsigned int no = 0;
+    KK_CUDA(cudaMemcpyAsync(&no, h->open_count, sizeof(no), cudaMemcpyDeviceToHost, s));
+    std::vector<int64_t> rows;
+    rc = collect_hist_rows(h, s, rows);
+    if (rc != KK_OK) return rc;
+    *n_open = no;
+    if ((int64_t)no > open_cap) return fail(KK_ERR_CAPACITY, "open-cluster buffer too small");
+    const int64_t nrows = (int64_t)rows.size() / 3;
+    *n_hist = nrows;
+    if (nrows > capacity || (!hist_out && nrows > 0)) return fail(KK_ERR_CAPACITY, "histogram buffer too small");
+    for (int64_t k = 0; k < nrows; ++k) {
+        hist_out[2 * k] = rows[3 * k + 1];
+        hist_out[2 * k + 1] = rows[3 * k + 2];
+    }
+    return KK_OK;
+}
+
+int kk_cluster_join(int64_t Lx, int64_t nslabs, const uint32_t* top_ids, const uint32_t* bot_ids,
+                    const int64_t* slab_offsets, const unsigned long long* sizes, int64_t n_nodes,
+                    int64_t* hist_out, int64_t capacity, int64_t* n_hist, void* stream) {
+    if (!n_hist || !slab_offsets || Lx <= 0 || nslabs <= 0 || n_nodes < 0 || n_nodes >= 0xFFFFFFFFll)
+        return fail(KK_ERR_ARG, "bad argument");
+    cudaStream_t s = S(stream);
+    uint32_t *par = nullptr, *off = nullptr;
+    unsigned long long *rsize = nullptr, *roots = nullptr;
+    unsigned int* nroots = nullptr;
+    const size_t n = (size_t)std::max<int64_t>(n_nodes, 1);
+    if (cudaMalloc(&par, 4 * n) || cudaMalloc(&rsize, 8 * n) || cudaMalloc(&roots, 8 * n) ||
+        cudaMalloc(&nroots, sizeof(unsigned int)) || cudaMalloc(&off, 4 * (size_t)nslabs)) {
+        cudaFree(par); cudaFree(rsize); cudaFree(roots); cudaFree(nroots); cudaFree(off);
+        cudaGetLastError();
+        return fail(KK_ERR_NOMEM, "join workspace");
+    }
+    std::vector<uint32_t> hoff(nslabs);
+    for (int64_t k = 0; k < nslabs; ++k) hoff[k] = (uint32_t)slab_offsets[k];
+    cudaError_t e = cudaMemcpyAsync(off, hoff.data(), 4 * (size_t)nslabs, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = launch_join(Lx, nslabs, top_ids, bot_ids, off, sizes, n_nodes, par, rsize, roots, nroots, s);
+    unsigned int nr = 0;
+    std::vector<unsigned long long> v;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&nr, nroots, sizeof(nr), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess && nr) {
+        v.resize(nr);
+        e = cudaMemcpyAsync(v.data(), roots, 8 * (size_t)nr, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    }
+    cudaFree(par); cudaFree(rsize); cudaFree(roots); cudaFree(nroots); cudaFree(off);
+    if (e != cudaSuccess) return fail(KK_ERR_CUDA, std::string("kk_cluster_join: ") + cudaGetErrorString(e));
+    std::sort(v.begin(), v.end());
+    std::vector<int64_t> rows;
+    for (size_t i = 0; i < v.size();) {
+        size_t j = i;
+        while (j < v.size() && v[j] == v[i]) ++j;
+        rows.push_back((int64_t)v[i]);
+        rows.push_back((int64_t)(j - i));
+        i = j;
+    }
+    *n_hist = (int64_t)rows.size() / 2;
+    if (*n_hist > capacity || (!hist_out && *n_hist > 0)) return fail(KK_ERR_CAPACITY, "histogram buffer too small");
+    if (!rows.empty()) std::memcpy(hist_out, rows.data(), sizeof(int64_t) * rows.size());
     return KK_OK;
 }
 

@@ -93,6 +93,12 @@ struct CclParams {
     unsigned long long* nbig;
     int64_t big_cap;
     int64_t node_cap;
+    int periodic_y;                // 0 for a row slab: no bonds across its top/bottom rows
+    uint32_t* open_flag;           // slab mode: [node] root touches the slab's top/bottom row
+    uint32_t* compact;             // slab mode: [node] root -> open-cluster index
+    unsigned long long* open_size; // slab mode: [open cluster] size
+    unsigned int* open_count;      // slab mode: device counter
+    int64_t open_cap;
 };
 
 __device__ __forceinline__ void hist_add(const CclParams& P, int64_t rep, unsigned long long s) {
@@ -268,18 +274,19 @@ __global__ void ccl_merge_kernel(const CclParams P) {
         const uint32_t* Er = P.edges + ((rep * P.tiles_y + ty) * P.tiles_x + txr) * kEdge;
         const uint32_t* Eb = P.edges + ((rep * P.tiles_y + tyb) * P.tiles_x + tx) * kEdge;
         const uint32_t* Ed = P.edges + ((rep * P.tiles_y + tyb) * P.tiles_x + txr) * kEdge;
+        const bool down_ok = P.periodic_y || ty + 1 < P.tiles_y;  // slab: no bond below its last row
         if (e < kTR) {  // right column row e: bonds (+1,0) and (+1,+1)
             if (e >= h_tile) continue;
             const uint32_t a = E[2 * kTX + kTR + e];
             if (a == kNone) continue;
             const uint32_t b = Er[2 * kTX + e];                       // (X1, y) = left col of right tile
             if (b != kNone) union32(P.node_par, a, b);
-            const uint32_t c = (e + 1 < h_tile) ? Er[2 * kTX + e + 1]  // (X1, y+1)
-                                                : Ed[2 * kTX + 0];     // wraps into the diagonal tile
+            const uint32_t c = (e + 1 < h_tile) ? Er[2 * kTX + e + 1]            // (X1, y+1)
+                                                : (down_ok ? Ed[2 * kTX + 0] : kNone);  // diagonal tile
             if (c != kNone) union32(P.node_par, a, c);
         } else {        // bottom row site x: bonds (0,+1) and (+1,+1)
             const int x = e - kTR;
-            if (x >= w_tile) continue;
+            if (x >= w_tile || !down_ok) continue;
             const uint32_t a = E[kTX + x];
             if (a == kNone) continue;
             const uint32_t b = Eb[x];                                  // (x, Y1) top row of tile below
@@ -308,6 +315,84 @@ __global__ void ccl_nodes_hist_rep_kernel(const CclParams P, const uint32_t* nod
     }
 }
 
+// ---- slab mode: roots touching the slab's first/last row stay open ------------
+__device__ __forceinline__ uint32_t edge_node(const CclParams& P, int64_t x, bool bottom) {
+    const int tx = (int)(x / kTX);
+    const int ty = bottom ? P.tiles_y - 1 : 0;
+    const uint32_t* E = P.edges + ((int64_t)ty * P.tiles_x + tx) * kEdge;
+    return E[(bottom ? kTX : 0) + (int)(x - (int64_t)tx * kTX)];
+}
+
+__global__ void ccl_slab_mark_kernel(const CclParams P) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 2 * P.g.Lx;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const bool bottom = i >= P.g.Lx;
+        const uint32_t n = edge_node(P, bottom ? i - P.g.Lx : i, bottom);
+        if (n != kNone) P.open_flag[find32(P.node_par, n)] = 1u;
+    }
+}
+
+__global__ void ccl_slab_hist_kernel(const CclParams P) {
+    const unsigned int n = (unsigned int)min64((int64_t)*P.node_count, P.node_cap);
+    for (unsigned int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        if (P.node_par[i] != i) continue;
+        if (P.open_flag[i]) {
+            const unsigned int c = atomicAdd(P.open_count, 1u);
+            P.compact[i] = c;
+            if ((int64_t)c < P.open_cap) P.open_size[c] = P.root_size[i];
+        } else {
+            hist_add(P, 0, P.root_size[i]);
+        }
+    }
+}
+
+__global__ void ccl_slab_ids_kernel(const CclParams P, uint32_t* top_ids, uint32_t* bot_ids) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 2 * P.g.Lx;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const bool bottom = i >= P.g.Lx;
+        const int64_t x = bottom ? i - P.g.Lx : i;
+        const uint32_t n = edge_node(P, x, bottom);
+        const uint32_t v = n == kNone ? kNone : P.compact[root_of(P.node_par, n)];
+        (bottom ? bot_ids : top_ids)[x] = v;
+    }
+}
+
+// ---- join of open clusters across slab boundaries (multi-GPU) -----------------
+// nodes: open clusters of all slabs (global ids); bonds: bottom row of slab s
+// to top row of slab (s+1) % nslabs, (0,+1) and (+1,+1).
+__global__ void join_init_kernel(uint32_t* par, unsigned long long* rsize, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        par[i] = (uint32_t)i;
+        rsize[i] = 0ull;
+    }
+}
+
+__global__ void join_union_kernel(uint32_t* par, const uint32_t* top, const uint32_t* bot, int64_t Lx,
+                                  int64_t nslabs, const uint32_t* off) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < Lx * nslabs;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = i / Lx, x = i - s * Lx;
+        const uint32_t a = bot[s * Lx + x];
+        if (a == kNone) continue;
+        const int64_t sn = (s + 1 == nslabs) ? 0 : s + 1;
+        const uint32_t b = top[sn * Lx + x];
+        if (b != kNone) union32(par, a + off[s], b + off[sn]);
+        const uint32_t c = top[sn * Lx + (x + 1 == Lx ? 0 : x + 1)];
+        if (c != kNone) union32(par, a + off[s], c + off[sn]);
+    }
+}
+
+__global__ void join_sum_kernel(uint32_t* par, const unsigned long long* size, unsigned long long* rsize, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(rsize + find32(par, (uint32_t)i), size[i]);
+}
+
+__global__ void join_roots_kernel(const uint32_t* par, const unsigned long long* rsize, int64_t n,
+                                  unsigned long long* out, unsigned int* nout) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        if (par[i] == (uint32_t)i) out[atomicAdd(nout, 1u)] = rsize[i];
+}
+
 int grid_for_n(int64_t n) {
     int64_t b = (n + 255) / 256;
     if (b > 148 * 16) b = 148 * 16;
@@ -330,8 +415,17 @@ int64_t ccl_node_cap(const Geom& g, int64_t replicas) { return ccl_tiles(g, repl
 cudaError_t launch_ccl(const uint32_t* lat, const Geom& g, int64_t replicas, int target, uint32_t* edges,
                        uint32_t* node_size, uint32_t* node_par, uint32_t* node_rep,
                        unsigned long long* root_size, unsigned int* counter, unsigned int* hist,
-                       unsigned long long* big, unsigned long long* nbig, int64_t big_cap, cudaStream_t s) {
+                       unsigned long long* big, unsigned long long* nbig, int64_t big_cap, cudaStream_t s,
+                       const SlabCclArgs* slab) {
     CclParams P{};
+    P.periodic_y = slab ? 0 : 1;
+    if (slab) {
+        P.open_flag = slab->open_flag;
+        P.compact = slab->compact;
+        P.open_size = slab->open_size;
+        P.open_count = slab->open_count;
+        P.open_cap = slab->open_cap;
+    }
     P.lat = lat;
     P.g = g;
     P.target = target;
@@ -364,8 +458,37 @@ cudaError_t launch_ccl(const uint32_t* lat, const Geom& g, int64_t replicas, int
     const int gn = grid_for_n(P.node_cap);
     ccl_nodes_sum_kernel<<<gn, 256, 0, s>>>(P);
     count_launch();
-    ccl_nodes_hist_rep_kernel<<<gn, 256, 0, s>>>(P, node_rep);
-    count_launch();
+    if (!slab) {
+        ccl_nodes_hist_rep_kernel<<<gn, 256, 0, s>>>(P, node_rep);
+        count_launch();
+        return cudaGetLastError();
+    }
+    e = cudaMemsetAsync(slab->open_flag, 0, sizeof(uint32_t) * (size_t)P.node_cap, s);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(slab->open_count, 0, sizeof(unsigned int), s);
+    if (e != cudaSuccess) return e;
+    const int ge = grid_for_n(2 * g.Lx);
+    ccl_slab_mark_kernel<<<ge, 256, 0, s>>>(P);
+    ccl_slab_hist_kernel<<<gn, 256, 0, s>>>(P);
+    ccl_slab_ids_kernel<<<ge, 256, 0, s>>>(P, slab->top_ids, slab->bot_ids);
+    for (int k = 0; k < 3; ++k) count_launch();
+    return cudaGetLastError();
+}
+
+// Merged sizes of open clusters joined across slab boundaries; writes the
+// roots' sizes to out (device, n entries max) and their count to nout.
+cudaError_t launch_join(int64_t Lx, int64_t nslabs, const uint32_t* top, const uint32_t* bot, const uint32_t* off,
+                        const unsigned long long* sizes, int64_t n, uint32_t* par, unsigned long long* rsize,
+                        unsigned long long* out, unsigned int* nout, cudaStream_t s) {
+    if (n == 0) return cudaMemsetAsync(nout, 0, sizeof(unsigned int), s);
+    const int gn = grid_for_n(n), gb = grid_for_n(Lx * nslabs);
+    cudaError_t e = cudaMemsetAsync(nout, 0, sizeof(unsigned int), s);
+    if (e != cudaSuccess) return e;
+    join_init_kernel<<<gn, 256, 0, s>>>(par, rsize, n);
+    join_union_kernel<<<gb, 256, 0, s>>>(par, top, bot, Lx, nslabs, off);
+    join_sum_kernel<<<gn, 256, 0, s>>>(par, sizes, rsize, n);
+    join_roots_kernel<<<gn, 256, 0, s>>>(par, rsize, n, out, nout);
+    for (int k = 0; k < 4; ++k) count_launch();
     return cudaGetLastError();
 }
 

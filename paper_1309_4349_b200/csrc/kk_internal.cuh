@@ -137,6 +137,17 @@ struct ObsParams {
 // Cluster sizes below kDense go to a dense per-replica histogram.
 constexpr int kDense = 4096;
 
+// Slab-mode cluster workspace (multi-GPU cluster histogram).
+struct SlabCclArgs {
+    uint32_t* open_flag;           // [node_cap]
+    uint32_t* compact;             // [node_cap]
+    unsigned long long* open_size; // [open_cap] (caller's device buffer)
+    unsigned int* open_count;      // device counter
+    int64_t open_cap;
+    uint32_t* top_ids;             // [Lx] caller's device buffer
+    uint32_t* bot_ids;             // [Lx]
+};
+
 // ---------------------------------------------------------------- launch counter
 void count_launch();
 

@@ -66,6 +66,13 @@ class TorchComm:
         self.dist.all_gather(outs, t, group=self.group)
         return np.concatenate([o.cpu().numpy()[: int(c.item())] for o, c in zip(outs, ns)], axis=0)
 
+    def all_gather_tensor(self, t):
+        if self.world == 1:
+            return [t]
+        outs = [self.torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(outs, t, group=self.group)
+        return outs
+
     def exchange_start(self, send_top, send_bot, recv_top, recv_bot):
         """send_top -> rank-1 (its bottom halo); send_bot -> rank+1 (its top halo)."""
         dist = self.dist
@@ -94,6 +101,7 @@ class GpuSlab:
         self.device = device
         self.hy = lat.halo_rows
         self.replicas = lat.replicas
+        self.Lx = lat.Lx
 
     def alloc_halo(self):
         return self.torch.zeros(self.replicas * self.hy * self.lat.W, dtype=self.torch.int32,
@@ -118,8 +126,25 @@ class GpuSlab:
     def stats(self, reset, stream):
         return self.lat.stats(reset, stream)
 
-    def cluster_histogram_raw(self, target, stream):
-        return self.lat.cluster_histogram_raw(target, stream=stream)
+    def cluster_histogram_rows(self, target, stream):
+        """Full periodic lattice: [(size, count)] of replica 0."""
+        return self.lat.cluster_histogram(target, stream=stream)[0]
+
+    # slab cluster histogram (multi-GPU)
+    def alloc_cluster_buffers(self):
+        t = self.torch
+        Lx = self.lat.Lx
+        cap = 2 * Lx + 16
+        return (t.empty(Lx, dtype=t.int32, device=self.device), t.empty(Lx, dtype=t.int32, device=self.device),
+                t.empty(cap, dtype=t.int64, device=self.device), cap)
+
+    def cluster_slab(self, target, bufs, stream):
+        top, bot, sizes, cap = bufs
+        return self.lat.cluster_slab(target, top.data_ptr(), bot.data_ptr(), sizes.data_ptr(), cap, stream)
+
+    def cluster_join(self, Lx, nslabs, top_all, bot_all, offsets, sizes_all, n_nodes, stream):
+        return kk.cluster_join(Lx, nslabs, top_all.data_ptr(), bot_all.data_ptr(), offsets,
+                               sizes_all.data_ptr(), n_nodes, stream)
 
     def close(self):
         self.lat.close()
@@ -197,9 +222,37 @@ class SlabDriver:
             self.comm.exchange_wait(self.comm.exchange_start(self.send_top, self.send_bot,
                                                              self.recv_top, self.recv_bot))
 
+    def cluster_histogram(self, target: int = 1):
+        """Cluster-size histogram [(size, count)] of the whole lattice (R9), on
+        rank 0 (None elsewhere).  Multi-GPU: slab-local labelling, open clusters
+        (touching a slab's first/last row) joined across slab boundaries on
+        rank 0."""
+        be = self.be
+        if self.world == 1:
+            return be.cluster_histogram_rows(target, self.stream)
+        if not hasattr(self, "_cbufs"):
+            self._cbufs = be.alloc_cluster_buffers()
+        rows, n_open = be.cluster_slab(target, self._cbufs, self.stream)
+        ns = self.comm.all_gather_rows(np.array([[n_open]], np.int64))[:, 0]
+        all_rows = self.comm.all_gather_rows(np.asarray(rows, np.int64).reshape(-1, 2))
+        tops = self.comm.all_gather_tensor(self._cbufs[0])
+        bots = self.comm.all_gather_tensor(self._cbufs[1])
+        sizes = self.comm.all_gather_tensor(self._cbufs[2])
+        if self.rank != 0:
+            return None
+        torch = self.comm.torch
+        offsets = np.concatenate([[0], np.cumsum(ns)[:-1]]).astype(np.int64)
+        sizes_all = torch.cat([sz[: int(n)] for sz, n in zip(sizes, ns)]) if int(ns.sum()) else sizes[0][:1]
+        jrows = be.cluster_join(be.Lx, self.world, torch.cat(tops), torch.cat(bots), offsets, sizes_all,
+                                int(ns.sum()), self.stream)
+        hist = {}
+        for sz, c in list(map(tuple, all_rows.tolist())) + list(map(tuple, np.asarray(jrows).tolist())):
+            hist[sz] = hist.get(sz, 0) + c
+        return sorted(hist.items())
+
     def observe(self, ccl: bool = True) -> dict:
-        """N_AB, composition and counters summed over slabs; cluster histogram
-        (single GPU: full lattice)."""
+        """N_AB, composition and counters summed over slabs, and the cluster
+        histogram of the A sites (R9)."""
         self.refresh_halos()
         nab = np.asarray(self.be.energy(self.recv_bot if self.world > 1 else None, self.stream), np.int64)
         na = np.asarray(self.be.composition(self.stream), np.int64)
@@ -210,10 +263,11 @@ class SlabDriver:
             st = self.comm.all_reduce_sum(st)
         out = {"n_ab": nab.tolist(), "n_a": na.tolist(), "attempted": st[:, 0].tolist(),
                "trivial": st[:, 1].tolist(), "accepted": st[:, 2].tolist(), "dnab_sum": st[:, 3].tolist()}
-        if ccl and self.world == 1:
-            h = self.be.cluster_histogram_raw(1, self.stream)
-            out["clusters_A"] = int(h[:, 2].sum()) if h.size else 0
-            out["largest_A"] = int(h[:, 1].max()) if h.size else 0
+        if ccl:
+            h = self.cluster_histogram(1)
+            if h is not None:
+                out["clusters_A"] = int(sum(c for _, c in h))
+                out["largest_A"] = int(max((sz for sz, _ in h), default=0))
         return out
 
 

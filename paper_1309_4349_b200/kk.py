@@ -46,6 +46,9 @@ SIGNATURES = {
     "kk_composition": (ctypes.c_int, [_p, _p, _p]),
     "kk_stats": (ctypes.c_int, [_p, _p, ctypes.c_int, _p]),
     "kk_cluster_histogram": (ctypes.c_int, [_p, ctypes.c_int, _p, _i64, ctypes.POINTER(_i64), _p]),
+    "kk_cluster_slab": (ctypes.c_int, [_p, ctypes.c_int, _p, _i64, ctypes.POINTER(_i64), _p, _p, _p, _i64,
+                                       ctypes.POINTER(_i64), _p]),
+    "kk_cluster_join": (ctypes.c_int, [_i64, _i64, _p, _p, _p, _p, _i64, _p, _i64, ctypes.POINTER(_i64), _p]),
     "kk_get_lattice": (ctypes.c_int, [_p, _p, _p]),
     "kk_set_lattice": (ctypes.c_int, [_p, _p, _p]),
     "kk_get_lattice_packed": (ctypes.c_int, [_p, _p, _p]),
@@ -97,6 +100,24 @@ def stream_ptr(stream) -> Optional[int]:
     if isinstance(stream, int):
         return stream
     return int(stream.cuda_stream)
+
+
+def cluster_join(Lx: int, nslabs: int, top_ids: int, bot_ids: int, offsets, sizes: int, n_nodes: int,
+                 stream=None):
+    """Merged open clusters across slab boundaries: rows [(size, count)]."""
+    lib = load()
+    n = _i64()
+    off = np.ascontiguousarray(offsets, np.int64)
+    cap = 4096
+    while True:
+        buf = np.zeros((cap, 2), np.int64)
+        rc = lib.kk_cluster_join(int(Lx), int(nslabs), top_ids, bot_ids, off.ctypes.data, sizes, int(n_nodes),
+                                 buf.ctypes.data, cap, ctypes.byref(n), stream_ptr(stream))
+        if rc == -4 and n.value > cap:
+            cap = int(n.value)
+            continue
+        _check(rc, "kk_cluster_join")
+        return buf[: n.value]
 
 
 def launch_count() -> int:
@@ -234,6 +255,22 @@ class Lattice:
         cut = np.ascontiguousarray(cut, np.int64)
         _check(load().kk_init_select_apply(self._h, K.ctypes.data, cut.ctypes.data, None),
                "kk_init_select_apply")
+
+    def cluster_slab(self, target: int, top_ids: int, bot_ids: int, open_sizes: int, open_cap: int,
+                     stream=None):
+        """Slab-local clusters: returns (complete rows [(size, count)], n_open)."""
+        lib = load()
+        nh, no = _i64(), _i64()
+        cap = 4096
+        while True:
+            buf = np.zeros((cap, 2), np.int64)
+            rc = lib.kk_cluster_slab(self._h, int(target), buf.ctypes.data, cap, ctypes.byref(nh), top_ids,
+                                     bot_ids, open_sizes, int(open_cap), ctypes.byref(no), stream_ptr(stream))
+            if rc == -4 and nh.value > cap:
+                cap = int(nh.value)
+                continue
+            _check(rc, "kk_cluster_slab")
+            return buf[: nh.value], int(no.value)
 
     def acceptance_table(self):
         out = np.zeros(7, np.uint32)

@@ -31,6 +31,7 @@ class OracleSlab:
         self.sweep, self.j = 0, 0
         self.st = np.zeros((1, 4), np.int64)
         self.replicas = 1
+        self.Lx = Lx
 
     # --- pass protocol
     def alloc_halo(self):
@@ -93,6 +94,75 @@ class OracleSlab:
             self.st[:] = 0
         return s
 
+    # --- slab cluster histogram (same contract as kk_cluster_slab / kk_cluster_join)
+    def alloc_cluster_buffers(self):
+        cap = 2 * self.Lx + 16
+        return (torch.zeros(self.Lx, dtype=torch.int32), torch.zeros(self.Lx, dtype=torch.int32),
+                torch.zeros(cap, dtype=torch.int64), cap)
+
+    def cluster_slab(self, target, bufs, stream):
+        top, bot, sizes, cap = bufs
+        lat, rows, Lx = self.cur, self.rows, self.Lx
+        lab = -np.ones((rows, Lx), np.int64)
+        comps = []
+        for y0 in range(rows):
+            for x0 in range(Lx):
+                if lat[y0, x0] != target or lab[y0, x0] >= 0:
+                    continue
+                stack, n, open_ = [(y0, x0)], 0, False
+                lab[y0, x0] = len(comps)
+                while stack:
+                    y, x = stack.pop()
+                    n += 1
+                    open_ |= (y == 0 or y == rows - 1)
+                    for dx, dy in [(1, 0), (1, 1), (0, 1), (-1, 0), (-1, -1), (0, -1)]:
+                        yy, xx = y + dy, (x + dx) % Lx
+                        if 0 <= yy < rows and lat[yy, xx] == target and lab[yy, xx] < 0:
+                            lab[yy, xx] = len(comps)
+                            stack.append((yy, xx))
+                comps.append((n, open_))
+        open_ids, complete = {}, {}
+        for c, (n, o) in enumerate(comps):
+            if o:
+                open_ids[c] = len(open_ids)
+                sizes[open_ids[c]] = n
+            else:
+                complete[n] = complete.get(n, 0) + 1
+        none = -1  # 0xFFFFFFFF as int32
+        top.copy_(torch.tensor([open_ids[l] if l >= 0 else none for l in lab[0]], dtype=torch.int32))
+        bot.copy_(torch.tensor([open_ids[l] if l >= 0 else none for l in lab[rows - 1]], dtype=torch.int32))
+        return np.array(sorted(complete.items()), np.int64).reshape(-1, 2), len(open_ids)
+
+    def cluster_join(self, Lx, nslabs, top_all, bot_all, offsets, sizes_all, n_nodes, stream):
+        par = list(range(n_nodes))
+
+        def find(a):
+            while par[a] != a:
+                a = par[a]
+            return a
+        top = top_all.numpy().reshape(nslabs, Lx)
+        bot = bot_all.numpy().reshape(nslabs, Lx)
+        for s in range(nslabs):
+            sn = (s + 1) % nslabs
+            for x in range(Lx):
+                a = bot[s, x]
+                if a < 0:
+                    continue
+                for b in (top[sn, x], top[sn, (x + 1) % Lx]):
+                    if b >= 0:
+                        ra, rb = find(a + offsets[s]), find(b + offsets[sn])
+                        if ra != rb:
+                            par[max(ra, rb)] = min(ra, rb)
+        tot = {}
+        sz = sizes_all.numpy()
+        for i in range(n_nodes):
+            r = find(i)
+            tot[r] = tot.get(r, 0) + int(sz[i])
+        h = {}
+        for v in tot.values():
+            h[v] = h.get(v, 0) + 1
+        return np.array(sorted(h.items()), np.int64).reshape(-1, 2)
+
     # --- distributed random start
     def _keys(self):
         k = np.zeros((self.rows, self.Lx), np.int64)
@@ -147,7 +217,8 @@ def _worker(rank, world, port, cfg, q):
         init = be.cur.copy()
         drv = SlabDriver(be, comm, rank, world)
         drv.sweep(n, T)
-        obs = drv.observe(ccl=False)
+        obs = drv.observe(ccl=True)
+        obs["hist"] = {t: drv.cluster_histogram(t) for t in (0, 1)}
         q.put((rank, init, be.cur.copy(), obs))
     finally:
         dist.destroy_process_group()
@@ -179,3 +250,8 @@ def test_slab_driver_matches_single_lattice(world, Lx, Ly, T, n):
     assert obs["n_a"] == [int(ref.sum())]
     assert obs["attempted"] == [st["attempted"]] and obs["accepted"] == [st["accepted"]]
     assert obs["trivial"] == [st["trivial"]] and obs["dnab_sum"] == [st["dnab_sum"]]
+    for t in (0, 1):                                     # slab-local labels + join == whole lattice
+        assert [tuple(r) for r in obs["hist"][t]] == O.cluster_histogram(ref, t)
+    assert obs["clusters_A"] == sum(c for _, c in O.cluster_histogram(ref, 1))
+    for r in res[1:]:
+        assert r[3]["hist"][1] is None                   # only rank 0 assembles the histogram
