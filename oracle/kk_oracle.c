@@ -255,17 +255,25 @@ void kko_schedule(uint64_t seed, uint32_t sweep, uint32_t replica, int ks[16]) {
 }
 
 /* Random draws of centre (x,y) in iteration j of sweep s (reading R6):
- * centre index i = (x - kx)/4 along its row, pair m = i>>1, slot i&1,
- * centre row l = (y - ky)/4; w = philox(ctr=(m, l, s, replica<<8 | j));
- * direction d = floor(w[2 slot] * 6 / 2^32), u32 = w[2 slot + 1]. */
+ * centre index i = (x - kx)/4 along its row, octet g = i >> 3 (8 consecutive
+ * centres), position p = i & 7, centre row l = (y - ky)/4; with
+ * c3 = replica<<8 | j:
+ *   direction: q = floor(philox(4g, l, s, c3)[p >> 1] * 36 / 2^32) encodes the
+ *     directions of the centre pair (p & ~1, p | 1): d = q / 6 for the even
+ *     position, d = q % 6 for the odd one (each uniform on 0..5 to 36/2^32);
+ *   acceptance: u32 = philox(4g + 1 + (p >> 2), l, s, c3)[p & 3]. */
 void kko_center_draw(uint64_t seed, uint32_t sweep, uint32_t replica, int j,
                      int kx, int ky, int64_t x, int64_t y, int* d, uint32_t* u32) {
     int64_t i = (x - kx) / 4, l = (y - ky) / 4;
+    int64_t g = i >> 3;
+    int p = (int)(i & 7);
+    uint32_t c3 = (replica << 8) | (uint32_t)j;
     uint32_t w[4];
-    philox_seeded((uint32_t)(i >> 1), (uint32_t)l, sweep, (replica << 8) | (uint32_t)j, seed, w);
-    int slot = (int)(i & 1);
-    *d = (int)(((uint64_t)w[2 * slot] * 6u) >> 32);
-    *u32 = w[2 * slot + 1];
+    philox_seeded((uint32_t)(4 * g), (uint32_t)l, sweep, c3, seed, w);
+    uint32_t q = (uint32_t)(((uint64_t)w[p >> 1] * 36u) >> 32);
+    *d = (p & 1) ? (int)(q % 6u) : (int)(q / 6u);
+    philox_seeded((uint32_t)(4 * g + 1 + (p >> 2)), (uint32_t)l, sweep, c3, seed, w);
+    *u32 = w[p & 3];
 }
 
 /* One MPKK sweep = one Monte Carlo step: 16 iterations;

@@ -129,7 +129,7 @@ void make_thresholds(double omega, uint32_t thr[7]) {
 
 void choose_tiles(kk_lattice* h) {
     const int twi_t = std::max(1, env_int("KK_TWI", 62));
-    const int thi_t = std::max(4, env_int("KK_THI", 160));
+    const int thi_t = std::max(4, env_int("KK_THI", 320));
     const int64_t W = h->g.W, rows = h->g.rows;
     const int64_t nx = (W + twi_t - 1) / twi_t;
     h->TWI = (int)((W + nx - 1) / nx);

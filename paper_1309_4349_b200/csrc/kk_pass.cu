@@ -29,7 +29,11 @@ namespace kk {
 
 namespace {
 
-constexpr int kThreads = 256;
+#ifndef KK_PASS_THREADS
+#define KK_PASS_THREADS 512
+#endif
+constexpr int kThreads = KK_PASS_THREADS;
+constexpr int kMinBlocks = 1024 / kThreads;  // 32 warps per SM at <= 64 registers
 constexpr uint32_t kNib = 0x11111111u;
 
 // Nibble-compressed bit plane of the sites at offset (DX, DY) from the centres
@@ -48,14 +52,16 @@ __device__ __forceinline__ uint32_t nib_view(uint32_t left, uint32_t mid, uint32
     return v & kNib;
 }
 
-// Four independent Philox4x32-10 streams, rounds interleaved for ILP; the
-// round keys come precomputed from the parameter bank (rk[0..9] for key
-// word 0, rk[10..19] for key word 1), so no per-item key schedule is issued.
-__device__ __forceinline__ void philox10_x4(const uint32_t m[4], uint32_t c1, uint32_t c2, uint32_t c3,
-                                            const uint32_t* rk, uint32_t out[4][4]) {
-    uint32_t a[4], b[4], c[4], d[4];
+// N independent Philox4x32-10 streams (counters m[k], c1, c2, c3), rounds
+// interleaved for ILP; the round keys come precomputed from the parameter bank
+// (rk[0..9] for key word 0, rk[10..19] for key word 1), so no per-item key
+// schedule is issued.
+template <int N>
+__device__ __forceinline__ void philox10_xn(const uint32_t m[N], uint32_t c1, uint32_t c2, uint32_t c3,
+                                            const uint32_t* rk, uint32_t out[N][4]) {
+    uint32_t a[N], b[N], c[N], d[N];
 #pragma unroll
-    for (int p = 0; p < 4; ++p) {
+    for (int p = 0; p < N; ++p) {
         a[p] = m[p];
         b[p] = c1;
         c[p] = c2;
@@ -64,7 +70,7 @@ __device__ __forceinline__ void philox10_x4(const uint32_t m[4], uint32_t c1, ui
 #pragma unroll
     for (int round = 0; round < 10; ++round) {
 #pragma unroll
-        for (int p = 0; p < 4; ++p) {
+        for (int p = 0; p < N; ++p) {
             const uint64_t p0 = (uint64_t)kPhiloxM0 * a[p];
             const uint64_t p1 = (uint64_t)kPhiloxM1 * c[p];
             const uint32_t na = (uint32_t)(p1 >> 32) ^ b[p] ^ rk[round];
@@ -76,7 +82,7 @@ __device__ __forceinline__ void philox10_x4(const uint32_t m[4], uint32_t c1, ui
         }
     }
 #pragma unroll
-    for (int p = 0; p < 4; ++p) {
+    for (int p = 0; p < N; ++p) {
         out[p][0] = a[p];
         out[p][1] = b[p];
         out[p][2] = c[p];
@@ -84,17 +90,39 @@ __device__ __forceinline__ void philox10_x4(const uint32_t m[4], uint32_t c1, ui
     }
 }
 
+// w[i] for a runtime i in 0..3 without local-memory indexing.
+__device__ __forceinline__ uint32_t sel4(const uint32_t w[4], uint32_t i) {
+    const uint32_t lo = (i & 1u) ? w[1] : w[0];
+    const uint32_t hi = (i & 1u) ? w[3] : w[2];
+    return (i & 2u) ? hi : lo;
+}
+
 struct Acc {
     uint32_t attempted, trivial, accepted;
-    int32_t dnab;
+    uint32_t idx_even, idx_odd;  // byte-lane sums of (v+3) over accepted centres (flushed every 32 items)
+    unsigned long long idx_sum;
 };
+
+__device__ __forceinline__ void acc_flush(Acc& a) {
+    a.idx_sum += ((a.idx_even & 0x00FF00FFu) + ((a.idx_even >> 8) & 0x00FF00FFu)) * 0x00010001u >> 16;
+    a.idx_sum += ((a.idx_odd & 0x00FF00FFu) + ((a.idx_odd >> 8) & 0x00FF00FFu)) * 0x00010001u >> 16;
+    a.idx_even = a.idx_odd = 0u;
+}
+
+// Predicated shared-memory XOR (no branch, no return value).
+__device__ __forceinline__ void red_xor_if(uint32_t* p, uint32_t v) {
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q red.shared.xor.b32 [%0], %1;\n\t}"
+                 :: "r"(a), "r"(v) : "memory");
+}
 
 struct Tabs {
     uint32_t* tile;            // H rows x WS words (col 0 and WS-1 are zero guards)
-    const uint4* mtab;         // [Wt] global pair indices of the word's 4 pairs
+    const uint2* mtab;         // [Wt] (global x of bit 0, word holds one aligned octet of centres)
+    uint32_t Lx;
     const uint32_t* wmask;     // [Wt] owned bits of the word (0 for halo words)
     const uint32_t* rowl;      // [H] centre-row index l | owned-row flag << 31
-    const uint32_t* thr;       // [8] thresholds
+    const uint2* thr2;         // [256] thresholds of the two nibbles of a byte of idx
     int WS;
 };
 
@@ -103,17 +131,40 @@ template <int KX>
 __device__ __forceinline__ void process_item(const Tabs& S, int r, int w, uint32_t sweep, uint32_t c3,
                                              const uint32_t* rk, Acc& acc) {
     const uint32_t rl = S.rowl[r];
-    const uint4 mq = S.mtab[w];
-    const uint32_t m[4] = {mq.x, mq.y, mq.z, mq.w};
-    uint32_t R4[4][4];
-    philox10_x4(m, rl & 0x7FFFFFFFu, sweep, c3, rk, R4);
+    const uint32_t l = rl & 0x7FFFFFFFu;
+    const uint2 mq = S.mtab[w];
+    // ---- random draws (R6): octet g of 8 centres; call 4g gives the four
+    // pair-direction words (q = w*36 >> 32 -> d_even = q/6, d_odd = q%6),
+    // calls 4g+1, 4g+2 the eight acceptance uniforms.
     uint32_t u[8];
     uint32_t dv = 0;  // direction nibble vector: nibble q = direction of centre q
+    if (mq.y) {       // the word is one whole octet (common case)
+        const uint32_t g4 = (mq.x >> 5) * 4u;
+        const uint32_t m[3] = {g4, g4 + 1u, g4 + 2u};
+        uint32_t R3[3][4];
+        philox10_xn<3>(m, l, sweep, c3, rk, R3);
 #pragma unroll
-    for (int p = 0; p < 4; ++p) {
-        dv |= (__umulhi(R4[p][0], 6u) << (8 * p)) | (__umulhi(R4[p][2], 6u) << (8 * p + 4));
-        u[2 * p] = R4[p][1];
-        u[2 * p + 1] = R4[p][3];
+        for (int p = 0; p < 4; ++p) {
+            const uint32_t q = __umulhi(R3[0][p], 36u);
+            const uint32_t de = (q * 43u) >> 8;  // q / 6 for q < 36
+            dv |= (de << (8 * p)) | ((q - 6u * de) << (8 * p + 4));
+            u[p] = R3[1][p];
+            u[4 + p] = R3[2][p];
+        }
+    } else {          // word straddles an octet boundary (x wrap, Lx % 32 != 0, tiny Lx)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            uint32_t x = mq.x + 4u * q + KX;
+            while (x >= S.Lx) x -= S.Lx;
+            const uint32_t i = (x - KX) >> 2, g4 = (i >> 3) * 4u, pos = i & 7u;
+            const uint32_t m2[2] = {g4, g4 + 1u + (pos >> 2)};
+            uint32_t R2[2][4];
+            philox10_xn<2>(m2, l, sweep, c3, rk, R2);
+            const uint32_t qq = __umulhi(sel4(R2[0], pos >> 1), 36u);
+            const uint32_t de = (qq * 43u) >> 8;
+            dv |= ((pos & 1u) ? (qq - 6u * de) : de) << (4 * q);
+            u[q] = sel4(R2[1], pos & 3u);
+        }
     }
 
     // ---- neighbourhood: rows r-2..r+2, columns w..w+2 (w+1 is the word itself)
@@ -165,55 +216,55 @@ __device__ __forceinline__ void process_item(const Tabs& S, int r, int w, uint32
     const uint32_t CA = c * 15u;
     const uint32_t idx = (E & CA) | ((0x66666666u - E) & ~CA);
 
-    // ---- Metropolis acceptance (integer thresholds, R5)
+    // ---- Metropolis acceptance (integer thresholds, R5): one 64-bit lookup
+    // per centre pair in a 256-entry table indexed by the byte of idx holding
+    // both centres' nibbles.
     uint32_t accb = 0;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-        const uint32_t iq = (idx >> (4 * q)) & 15u;
-        accb |= (u[q] <= S.thr[iq] ? 1u : 0u) << (4 * q);
+    for (int p = 0; p < 4; ++p) {
+        const uint32_t byte = __byte_perm(idx, 0u, 0x4440u | (uint32_t)p);
+        const uint2 t2 = S.thr2[byte];
+        accb += (u[2 * p] <= t2.x ? 1u : 0u) << (8 * p);
+        accb += (u[2 * p + 1] <= t2.y ? 1u : 0u) << (8 * p + 4);
     }
     const uint32_t AN = accb & Dsel;
 
-    // ---- flips (XOR masks; only words with changes are touched)
-    const uint32_t nb0 = ~b0 & kNib, nb1 = ~b1 & kNib, nb2 = ~b2 & kNib;
-    const uint32_t A0 = AN & nb2 & nb1;  // directions 0,1
-    const uint32_t A2 = AN & nb2 & b1;   // directions 2,3
-    const uint32_t A4 = AN & b2 & nb1;   // directions 4,5
-    const uint32_t P0 = (A0 & nb0) << KX;  // (+1, 0)
-    const uint32_t P1 = (A0 & b0) << KX;   // (+1,+1)
-    const uint32_t P2 = (A2 & nb0) << KX;  // ( 0,+1)
-    const uint32_t P3 = (A2 & b0) << KX;   // (-1, 0)
-    const uint32_t P4 = (A4 & nb0) << KX;  // (-1,-1)
-    const uint32_t P5 = (A4 & b0) << KX;   // ( 0,-1)
-    const uint32_t Fr = (AN << KX) | (P0 << 1) | (P3 >> 1);
-    const uint32_t Fu = (P1 << 1) | P2;
-    const uint32_t Fd = (P4 >> 1) | P5;
+    // ---- flips (XOR masks).  Directions by row: d=0 (+1,0) and d=3 (-1,0)
+    // stay in row r, d=1 (+1,+1) and d=2 (0,+1) go to r+1, d=4 (-1,-1) and
+    // d=5 (0,-1) to r-1; d = 4 b2 + 2 b1 + b0.
+    const uint32_t x01 = b1 ^ b0;
+    const uint32_t up = AN & ~b2 & x01;         // d in {1,2}
+    const uint32_t dn = AN & b2 & ~b1;          // d in {4,5}
+    const uint32_t same = AN & ~b2 & ~x01;      // d in {0,3}
+    const uint32_t U1 = up & b0;                // (+1,+1)
+    const uint32_t D4 = dn & ~b0;               // (-1,-1)
+    const uint32_t R0 = same & ~b0;             // (+1, 0)
+    const uint32_t R3 = same & b0;              // (-1, 0)
+    const uint32_t Fr = (AN << KX) | (R0 << (KX + 1)) | ((R3 << KX) >> 1);
+    const uint32_t Fu = ((up ^ U1) << KX) | (U1 << (KX + 1));
+    const uint32_t Fd = ((dn ^ D4) << KX) | ((D4 << KX) >> 1);
     uint32_t* row = S.tile + r * S.WS + w + 1;
-    if (Fr) atomicXor(row, Fr);
-    if (Fu) atomicXor(row + S.WS, Fu);
-    if (Fd) atomicXor(row - S.WS, Fd);
+    red_xor_if(row, Fr);
+    red_xor_if(row + S.WS, Fu);
+    red_xor_if(row - S.WS, Fd);
     if constexpr (KX == 3) {  // centre at bit 31 moving right: partner in the next word
-        if (P0 >> 31) atomicXor(row + 1, 1u);
-        if (P1 >> 31) atomicXor(row + S.WS + 1, 1u);
+        red_xor_if(row + 1, R0 >> 28);
+        red_xor_if(row + S.WS + 1, U1 >> 28);
     }
     if constexpr (KX == 0) {  // centre at bit 0 moving left: partner in the previous word
-        if (P3 & 1u) atomicXor(row - 1, 0x80000000u);
-        if (P4 & 1u) atomicXor(row - S.WS - 1, 0x80000000u);
+        red_xor_if(row - 1, (R3 & 1u) << 31);
+        red_xor_if(row - S.WS - 1, (D4 & 1u) << 31);
     }
 
-    // ---- counters over owned centres
+    // ---- counters over owned centres (branch-free; in_mask = 0 for halo)
     const uint32_t in_mask = (rl >> 31) ? ((S.wmask[w] >> KX) & kNib) : 0u;
-    if (in_mask) {
-        const uint32_t A = AN & in_mask;
-        const uint32_t na = __popc(A);
-        acc.attempted += __popc(in_mask);
-        acc.trivial += __popc(in_mask & ~Dsel);
-        acc.accepted += na;
-        const uint32_t Sg = idx & (A * 15u);
-        const uint32_t s8 = (Sg & 0x0F0F0F0Fu) + ((Sg >> 4) & 0x0F0F0F0Fu);
-        const uint32_t sum = (s8 * 0x01010101u) >> 24;
-        acc.dnab += 2 * ((int32_t)sum - 3 * (int32_t)na);
-    }
+    const uint32_t A = AN & in_mask;
+    acc.attempted += __popc(in_mask);
+    acc.trivial += __popc(in_mask & ~Dsel);
+    acc.accepted += __popc(A);
+    const uint32_t Sg = idx & (A * 15u);
+    acc.idx_even += Sg & 0x0F0F0F0Fu;   // byte lanes: <= 6 per item per lane
+    acc.idx_odd += (Sg >> 4) & 0x0F0F0F0Fu;
 }
 
 template <int KX>
@@ -224,8 +275,13 @@ __device__ __forceinline__ void run_iteration(const Tabs& S, int Wt, int r_first
     int a = threadIdx.x / Wt;
     int w = threadIdx.x - a * Wt;
     const int da = kThreads / Wt, dw = kThreads - da * Wt;
+    int since_flush = 0;
     for (int it = threadIdx.x; it < items; it += kThreads) {
         process_item<KX>(S, r_first + 4 * a, w, sweep, c3, rk, acc);
+        if (++since_flush == 32) {
+            acc_flush(acc);
+            since_flush = 0;
+        }
         a += da;
         w += dw;
         if (w >= Wt) {
@@ -236,9 +292,9 @@ __device__ __forceinline__ void run_iteration(const Tabs& S, int Wt, int r_first
 }
 
 template <int T>
-__global__ void __launch_bounds__(kThreads, 4) pass_kernel(const PassParams P) {
+__global__ void __launch_bounds__(kThreads, kMinBlocks) pass_kernel(const PassParams P) {
     extern __shared__ uint32_t smem[];
-    __shared__ uint32_t thr[8];
+    __shared__ uint2 thr2[256];
     __shared__ unsigned long long red[4][kThreads / 32];
     constexpr int HY = 3 * T;
     const int rep = blockIdx.z;
@@ -254,19 +310,17 @@ __global__ void __launch_bounds__(kThreads, 4) pass_kernel(const PassParams P) {
     const uint32_t* hbot = P.halo_bot ? P.halo_bot + rep * P.halo_rep_words : nullptr;
 
     uint32_t* tile = smem;                                        // [H][WS]
-    uint4* mtab = reinterpret_cast<uint4*>(tile + ((H * WS + 3) & ~3));  // [Wt], 16-byte aligned
+    uint2* mtab = reinterpret_cast<uint2*>(tile + ((H * WS + 3) & ~3));  // [Wt], 8-byte aligned
     uint32_t* wmask = reinterpret_cast<uint32_t*>(mtab + Wt);     // [Wt]
     uint32_t* rowl = wmask + Wt;                                  // [H]
-    if (threadIdx.x < 7) thr[threadIdx.x] = P.thr[threadIdx.x];
+    for (int b = threadIdx.x; b < 256; b += kThreads)
+        thr2[b] = make_uint2(P.thr[min(b & 15, 6)], P.thr[min(b >> 4, 6)]);
 
     // ---- per-pass tables
-    const int64_t m_wrap = g.Lx >> 3;
     for (int w = threadIdx.x; w < Wt; w += kThreads) {
         const int64_t xu = X0 - 32 + 32 * (int64_t)w;  // unwrapped x of bit 0
         const int64_t xg = wrap_mod(xu, g.Lx);
-        uint32_t mm[4];
-        for (int p = 0; p < 4; ++p) mm[p] = (uint32_t)(((xg >> 3) + p) % m_wrap);
-        mtab[w] = make_uint4(mm[0], mm[1], mm[2], mm[3]);
+        mtab[w] = make_uint2((uint32_t)xg, ((xg & 31) == 0 && xg + 32 <= g.Lx) ? 1u : 0u);
         uint32_t own = 0;
         if (w >= 1 && w <= P.TWI && xu < g.Lx) {
             const int64_t nbits = g.Lx - xu;
@@ -313,13 +367,14 @@ __global__ void __launch_bounds__(kThreads, 4) pass_kernel(const PassParams P) {
     __syncthreads();
 
     const Words4 sched = philox10(0u, 0u, P.sweep, ((uint32_t)rep << 8) | kTagSchedule, P.key0, P.key1);
-    Acc acc = {0u, 0u, 0u, 0};
+    Acc acc = {0u, 0u, 0u, 0u, 0u, 0ull};
     Tabs S;
     S.tile = tile;
     S.mtab = mtab;
+    S.Lx = (uint32_t)g.Lx;
     S.wmask = wmask;
     S.rowl = rowl;
-    S.thr = thr;
+    S.thr2 = thr2;
     S.WS = WS;
     const int phase0 = (int)((Y0 - HY + g.y_begin) & 3);
 
@@ -342,6 +397,7 @@ __global__ void __launch_bounds__(kThreads, 4) pass_kernel(const PassParams P) {
             case 2: run_iteration<2>(S, Wt, r_first, nrows, P.sweep, c3, P.rk, acc); break;
             default: run_iteration<3>(S, Wt, r_first, nrows, P.sweep, c3, P.rk, acc); break;
         }
+        acc_flush(acc);
         __syncthreads();
     }
 
@@ -359,7 +415,8 @@ __global__ void __launch_bounds__(kThreads, 4) pass_kernel(const PassParams P) {
 
     // ---- counters: warp reduce, block reduce, one atomic per CTA per counter
     unsigned long long v0 = acc.attempted, v1 = acc.trivial, v2 = acc.accepted;
-    long long v3 = acc.dnab;
+    // sum over accepted owned centres of dN_AB = 2 v = 2 (idx - 3)
+    long long v3 = 2 * ((long long)acc.idx_sum - 3 * (long long)acc.accepted);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         v0 += __shfl_xor_sync(0xFFFFFFFFu, v0, o);
@@ -387,7 +444,7 @@ int pass_smem_bytes(int T, int THI, int TWI) {
     const int H = THI + 6 * T, Wt = TWI + 2, WS = Wt + 2;
     int tile_bytes = H * WS * 4;
     tile_bytes = (tile_bytes + 15) / 16 * 16;
-    return tile_bytes + Wt * 16 + Wt * 4 + H * 4;
+    return tile_bytes + Wt * 8 + Wt * 4 + H * 4;
 }
 
 cudaError_t launch_pass(int T, const PassParams& P, int grid_y, int replicas, cudaStream_t stream) {

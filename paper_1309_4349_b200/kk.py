@@ -72,9 +72,12 @@ SIGNATURES = {
 _lib = None
 
 
-def load(path: str = LIB_PATH):
-    """Load libkk.so (raises if it was not built — no fallback)."""
+def load(path: str = None):
+    """Load libkk.so (raises if it was not built — no fallback).  KK_LIB may
+    point at an alternative build of the same library (tuning experiments)."""
     global _lib
+    if path is None:
+        path = os.environ.get("KK_LIB", LIB_PATH)
     if _lib is None:
         if not os.path.exists(path):
             raise KKError(f"{path} not found: build it with `python -m paper_1309_4349_b200.build`")

@@ -66,17 +66,22 @@ def test_philox_matches_triton_interpreter(seed):
 
 def test_schedule_and_draw_layout():
     """k_j are the 16 nibbles of words 0,1 of philox((0,0,s,tag 0x10)); the
-    centre draw uses pair/slot words (reading R6) — checked against Philox."""
+    centre draw (reading R6) takes the pair's direction word from
+    philox(4g, l, s, c3)[p>>1] split as q = w*36>>32 -> (q/6, q%6) and u32
+    from philox(4g+1+(p>>2), l, s, c3)[p&3] — checked against Philox."""
     seed, s = 987654321, 17
-    w = O.philox4x32_10((0, 0, s, 0x10), (seed & 0xFFFFFFFF, seed >> 32))
+    key = (seed & 0xFFFFFFFF, seed >> 32)
+    w = O.philox4x32_10((0, 0, s, 0x10), key)
     ks = O.schedule(seed, s)
     assert ks == [(w[j // 8] >> (4 * (j % 8))) & 15 for j in range(16)]
-    # centre x = 4*i + kx, y = 4*l + ky; pair m = i >> 1, slot = i & 1
-    for (x, y, kx, ky, j) in [(1, 2, 1, 2, 3), (5, 2, 1, 2, 3), (12, 8, 0, 0, 15), (31, 35, 3, 3, 0)]:
+    for (x, y, kx, ky, j) in [(1, 2, 1, 2, 3), (5, 2, 1, 2, 3), (12, 8, 0, 0, 15), (31, 35, 3, 3, 0),
+                              (157, 6, 1, 2, 9), (4096 + 28, 40, 0, 0, 7)]:
         i, l = (x - kx) // 4, (y - ky) // 4
-        w = O.philox4x32_10((i >> 1, l, s, (2 << 8) | j), (seed & 0xFFFFFFFF, seed >> 32))
-        d, u = O.center_draw(seed, s, 2, j, kx, ky, x, y)
-        slot = i & 1
-        assert d == (w[2 * slot] * 6) >> 32
-        assert u == w[2 * slot + 1]
+        g, p = i >> 3, i & 7
+        c3 = (2 << 8) | j
+        q = (O.philox4x32_10((4 * g, l, s, c3), key)[p >> 1] * 36) >> 32
+        u = O.philox4x32_10((4 * g + 1 + (p >> 2), l, s, c3), key)[p & 3]
+        d, uu = O.center_draw(seed, s, 2, j, kx, ky, x, y)
+        assert d == (q % 6 if p & 1 else q // 6)
+        assert uu == u
         assert 0 <= d < 6
