@@ -24,7 +24,7 @@
  *  - Return value: KK_OK (0) or a negative kk_status; the last error message of
  *    the calling thread is available from kk_last_error().  No call aborts the
  *    process; CUDA errors are reported as KK_ERR_CUDA.
- *  - Requirements (R10): Lx % 8 == 0, Ly % 4 == 0, Lx >= 8, Ly >= 4.
+ *  - Requirements (R10): Lx % 4 == 0, Ly % 4 == 0, Lx >= 4, Ly >= 4.
  */
 #ifndef KK_H_
 #define KK_H_
@@ -56,7 +56,7 @@ typedef enum {
 } kk_init_mode;
 
 typedef struct {
-    int64_t Lx;             /* row length (sites), multiple of 8 */
+    int64_t Lx;             /* row length (sites), multiple of 4 */
     int64_t Ly;             /* rows of the FULL lattice, multiple of 4 */
     int64_t y_begin;        /* first global row held by this handle (slab), multiple of 4 */
     int64_t y_count;        /* rows held (slab height), multiple of 4; = Ly for a full lattice */

@@ -128,7 +128,7 @@ void make_thresholds(double omega, uint32_t thr[7]) {
 }
 
 void choose_tiles(kk_lattice* h) {
-    const int twi_t = std::max(1, env_int("KK_TWI", 62));
+    const int twi_t = std::max(1, env_int("KK_TWI", 64));
     const int thi_t = std::max(4, env_int("KK_THI", 320));
     const int64_t W = h->g.W, rows = h->g.rows;
     const int64_t nx = (W + twi_t - 1) / twi_t;
@@ -346,7 +346,7 @@ int64_t kk_launch_count(void) { return (int64_t)g_launches.load(); }
 int kk_create_ex(kk_handle* out, const kk_config* c) {
     if (!out || !c) return fail(KK_ERR_ARG, "null argument");
     *out = nullptr;
-    if (c->Lx < 8 || c->Lx % 8) return fail(KK_ERR_ARG, "Lx must be a positive multiple of 8 (DESIGN.md R10)");
+    if (c->Lx < 4 || c->Lx % 4) return fail(KK_ERR_ARG, "Lx must be a positive multiple of 4 (DESIGN.md R10)");
     if (c->Ly < 4 || c->Ly % 4) return fail(KK_ERR_ARG, "Ly must be a positive multiple of 4 (DESIGN.md R10)");
     if (c->y_count < 4 || c->y_count % 4 || c->y_begin < 0 || c->y_begin % 4 || c->y_begin + c->y_count > c->Ly)
         return fail(KK_ERR_ARG, "slab [y_begin, y_begin+y_count) must be inside [0, Ly) in multiples of 4");

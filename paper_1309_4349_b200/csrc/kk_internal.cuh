@@ -48,7 +48,7 @@ constexpr uint32_t kTagInit = 0x20u;
 // Device lattice layout (include/kk.h): per replica `rows` rows of W uint32
 // words, site x of a row is bit x%32 of word x/32, bits >= Lx are zero.
 struct Geom {
-    int64_t Lx;         // sites per row (multiple of 8)
+    int64_t Lx;         // sites per row (multiple of 4)
     int64_t rows;       // rows held by this handle (slab height)
     int64_t y_begin;    // global row of local row 0
     int64_t Ly;         // rows of the full lattice

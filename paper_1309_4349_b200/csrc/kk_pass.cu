@@ -109,20 +109,19 @@ __device__ __forceinline__ void acc_flush(Acc& a) {
     a.idx_even = a.idx_odd = 0u;
 }
 
-// Predicated shared-memory XOR (no branch, no return value).
-__device__ __forceinline__ void red_xor_if(uint32_t* p, uint32_t v) {
-    const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q red.shared.xor.b32 [%0], %1;\n\t}"
-                 :: "r"(a), "r"(v) : "memory");
-}
+
+// Dynamic shared memory: the tile (H rows x WS words; columns 0 and WS-1 are
+// zero guards) at offset 0, then the per-pass tables.  Addressed through the
+// shared-space symbol so every access compiles to LDS/ATOMS with no generic
+// pointer conversion.
+extern __shared__ uint32_t kk_smem[];
+__shared__ uint2 kk_thr2[256];  // thresholds of the two nibbles of a byte of idx
 
 struct Tabs {
-    uint32_t* tile;            // H rows x WS words (col 0 and WS-1 are zero guards)
-    const uint2* mtab;         // [Wt] (global x of bit 0, word holds one aligned octet of centres)
+    int mt_off;                // uint2 [Wt]: (global x of bit 0, word holds one aligned octet of centres)
+    int wm_off;                // uint32 [Wt]: owned bits of the word (0 for halo words)
+    int rl_off;                // uint32 [H]: centre-row index l | owned-row flag << 31
     uint32_t Lx;
-    const uint32_t* wmask;     // [Wt] owned bits of the word (0 for halo words)
-    const uint32_t* rowl;      // [H] centre-row index l | owned-row flag << 31
-    const uint2* thr2;         // [256] thresholds of the two nibbles of a byte of idx
     int WS;
 };
 
@@ -130,9 +129,9 @@ struct Tabs {
 template <int KX>
 __device__ __forceinline__ void process_item(const Tabs& S, int r, int w, uint32_t sweep, uint32_t c3,
                                              const uint32_t* rk, Acc& acc) {
-    const uint32_t rl = S.rowl[r];
+    const uint32_t rl = kk_smem[S.rl_off + r];
     const uint32_t l = rl & 0x7FFFFFFFu;
-    const uint2 mq = S.mtab[w];
+    const uint2 mq = reinterpret_cast<const uint2*>(kk_smem + S.mt_off)[w];
     // ---- random draws (R6): octet g of 8 centres; call 4g gives the four
     // pair-direction words (q = w*36 >> 32 -> d_even = q/6, d_odd = q%6),
     // calls 4g+1, 4g+2 the eight acceptance uniforms.
@@ -168,13 +167,13 @@ __device__ __forceinline__ void process_item(const Tabs& S, int r, int w, uint32
     }
 
     // ---- neighbourhood: rows r-2..r+2, columns w..w+2 (w+1 is the word itself)
-    const uint32_t* t = S.tile + (r - 2) * S.WS + w;
+    const int t0 = (r - 2) * S.WS + w;
     uint32_t L[5], M[5], R[5];
 #pragma unroll
     for (int k = 0; k < 5; ++k) {
-        L[k] = t[k * S.WS];
-        M[k] = t[k * S.WS + 1];
-        R[k] = t[k * S.WS + 2];
+        L[k] = kk_smem[t0 + k * S.WS];
+        M[k] = kk_smem[t0 + k * S.WS + 1];
+        R[k] = kk_smem[t0 + k * S.WS + 2];
     }
 #define NV(dx, dy) nib_view<KX, dx>(L[(dy) + 2], M[(dy) + 2], R[(dy) + 2])
     const uint32_t c = NV(0, 0);
@@ -223,7 +222,7 @@ __device__ __forceinline__ void process_item(const Tabs& S, int r, int w, uint32
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
         const uint32_t byte = __byte_perm(idx, 0u, 0x4440u | (uint32_t)p);
-        const uint2 t2 = S.thr2[byte];
+        const uint2 t2 = kk_thr2[byte];
         accb += (u[2 * p] <= t2.x ? 1u : 0u) << (8 * p);
         accb += (u[2 * p + 1] <= t2.y ? 1u : 0u) << (8 * p + 4);
     }
@@ -243,21 +242,21 @@ __device__ __forceinline__ void process_item(const Tabs& S, int r, int w, uint32
     const uint32_t Fr = (AN << KX) | (R0 << (KX + 1)) | ((R3 << KX) >> 1);
     const uint32_t Fu = ((up ^ U1) << KX) | (U1 << (KX + 1));
     const uint32_t Fd = ((dn ^ D4) << KX) | ((D4 << KX) >> 1);
-    uint32_t* row = S.tile + r * S.WS + w + 1;
-    red_xor_if(row, Fr);
-    red_xor_if(row + S.WS, Fu);
-    red_xor_if(row - S.WS, Fd);
+    const int ro = r * S.WS + w + 1;
+    if (Fr) atomicXor(&kk_smem[ro], Fr);
+    if (Fu) atomicXor(&kk_smem[ro + S.WS], Fu);
+    if (Fd) atomicXor(&kk_smem[ro - S.WS], Fd);
     if constexpr (KX == 3) {  // centre at bit 31 moving right: partner in the next word
-        red_xor_if(row + 1, R0 >> 28);
-        red_xor_if(row + S.WS + 1, U1 >> 28);
+        if (R0 >> 28) atomicXor(&kk_smem[ro + 1], 1u);
+        if (U1 >> 28) atomicXor(&kk_smem[ro + S.WS + 1], 1u);
     }
     if constexpr (KX == 0) {  // centre at bit 0 moving left: partner in the previous word
-        red_xor_if(row - 1, (R3 & 1u) << 31);
-        red_xor_if(row - S.WS - 1, (D4 & 1u) << 31);
+        if (R3 & 1u) atomicXor(&kk_smem[ro - 1], 0x80000000u);
+        if (D4 & 1u) atomicXor(&kk_smem[ro - S.WS - 1], 0x80000000u);
     }
 
     // ---- counters over owned centres (branch-free; in_mask = 0 for halo)
-    const uint32_t in_mask = (rl >> 31) ? ((S.wmask[w] >> KX) & kNib) : 0u;
+    const uint32_t in_mask = (rl >> 31) ? ((kk_smem[S.wm_off + w] >> KX) & kNib) : 0u;
     const uint32_t A = AN & in_mask;
     acc.attempted += __popc(in_mask);
     acc.trivial += __popc(in_mask & ~Dsel);
@@ -293,8 +292,6 @@ __device__ __forceinline__ void run_iteration(const Tabs& S, int Wt, int r_first
 
 template <int T>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) pass_kernel(const PassParams P) {
-    extern __shared__ uint32_t smem[];
-    __shared__ uint2 thr2[256];
     __shared__ unsigned long long red[4][kThreads / 32];
     constexpr int HY = 3 * T;
     const int rep = blockIdx.z;
@@ -309,12 +306,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) pass_kernel(const PassPa
     const uint32_t* htop = P.halo_top ? P.halo_top + rep * P.halo_rep_words : nullptr;
     const uint32_t* hbot = P.halo_bot ? P.halo_bot + rep * P.halo_rep_words : nullptr;
 
-    uint32_t* tile = smem;                                        // [H][WS]
-    uint2* mtab = reinterpret_cast<uint2*>(tile + ((H * WS + 3) & ~3));  // [Wt], 8-byte aligned
-    uint32_t* wmask = reinterpret_cast<uint32_t*>(mtab + Wt);     // [Wt]
-    uint32_t* rowl = wmask + Wt;                                  // [H]
+    Tabs S;
+    S.WS = WS;
+    S.Lx = (uint32_t)g.Lx;
+    S.mt_off = (H * WS + 1) & ~1;     // uint2 table, 8-byte aligned
+    S.wm_off = S.mt_off + 2 * Wt;
+    S.rl_off = S.wm_off + Wt;
+    uint2* mtab = reinterpret_cast<uint2*>(kk_smem + S.mt_off);
     for (int b = threadIdx.x; b < 256; b += kThreads)
-        thr2[b] = make_uint2(P.thr[min(b & 15, 6)], P.thr[min(b >> 4, 6)]);
+        kk_thr2[b] = make_uint2(P.thr[min(b & 15, 6)], P.thr[min(b >> 4, 6)]);
 
     // ---- per-pass tables
     for (int w = threadIdx.x; w < Wt; w += kThreads) {
@@ -326,30 +326,36 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) pass_kernel(const PassPa
             const int64_t nbits = g.Lx - xu;
             own = nbits >= 32 ? 0xFFFFFFFFu : ((1u << nbits) - 1u);
         }
-        wmask[w] = own;
+        kk_smem[S.wm_off + w] = own;
     }
     for (int r = threadIdx.x; r < H; r += kThreads) {
         const int64_t y_local = Y0 - HY + r;
         const int64_t yg = wrap_mod(g.y_begin + y_local, g.Ly);
         const bool owned = r >= HY && r < HY + P.THI && y_local < g.rows;
-        rowl[r] = (uint32_t)(yg >> 2) | (owned ? 0x80000000u : 0u);
+        kk_smem[S.rl_off + r] = (uint32_t)(yg >> 2) | (owned ? 0x80000000u : 0u);
     }
 
     // ---- stage tile + halo (coalesced 32-bit loads, periodic in x)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const bool fast_x = (g.tail == 0);
     const int64_t gw0 = X0 / 32 - 1;
+    // no x wrap and whole words: plain contiguous row copies
+    const bool contiguous = g.tail == 0 && gw0 >= 0 && gw0 + Wt <= g.W;
     for (int r = warp; r < H; r += kThreads / 32) {
         const uint32_t* row = row_source(g, src, htop, hbot, HY, Y0 - HY + r);
-        uint32_t* trow = tile + r * WS;
+        const int trow = r * WS;
         if (lane == 0) {
-            trow[0] = 0u;
-            trow[WS - 1] = 0u;
+            kk_smem[trow] = 0u;
+            kk_smem[trow + WS - 1] = 0u;
+        }
+        if (contiguous && row) {
+            const uint32_t* rp = row + gw0;
+            for (int w = lane; w < Wt; w += 32) kk_smem[trow + 1 + w] = rp[w];
+            continue;
         }
         for (int w = lane; w < Wt; w += 32) {
             uint32_t v = 0;
             if (row) {
-                if (fast_x) {
+                if (g.tail == 0) {
                     int64_t gw = gw0 + w;
                     while (gw < 0) gw += g.W;
                     while (gw >= g.W) gw -= g.W;
@@ -361,21 +367,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) pass_kernel(const PassPa
                     v = get32(row, p, g);
                 }
             }
-            trow[w + 1] = v;
+            kk_smem[trow + 1 + w] = v;
         }
     }
     __syncthreads();
 
     const Words4 sched = philox10(0u, 0u, P.sweep, ((uint32_t)rep << 8) | kTagSchedule, P.key0, P.key1);
     Acc acc = {0u, 0u, 0u, 0u, 0u, 0ull};
-    Tabs S;
-    S.tile = tile;
-    S.mtab = mtab;
-    S.Lx = (uint32_t)g.Lx;
-    S.wmask = wmask;
-    S.rowl = rowl;
-    S.thr2 = thr2;
-    S.WS = WS;
     const int phase0 = (int)((Y0 - HY + g.y_begin) & 3);
 
 #pragma unroll 1
@@ -402,15 +400,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) pass_kernel(const PassPa
     }
 
     // ---- write the interior to the other buffer
-    uint32_t* dst = P.dst + rep * g.rep_words;
-    for (int r = HY + warp; r < HY + P.THI; r += kThreads / 32) {
-        const int64_t y = Y0 + (r - HY);
-        if (y >= g.rows) break;
-        for (int w = 1 + lane; w <= P.TWI; w += 32) {
-            const int64_t gw = X0 / 32 + (w - 1);
-            if (gw >= g.W) break;
-            dst[y * g.W + gw] = tile[r * WS + w + 1] & word_mask(g, gw);
-        }
+    const int rows_out = (int)min64(P.THI, g.rows - Y0);
+    const int words_out = (int)min64(P.TWI, g.W - X0 / 32);
+    uint32_t* dst = P.dst + rep * g.rep_words + Y0 * g.W + X0 / 32;
+    const uint32_t last_mask = (X0 / 32 + words_out == g.W) ? word_mask(g, g.W - 1) : 0xFFFFFFFFu;
+    for (int r = warp; r < rows_out; r += kThreads / 32) {
+        uint32_t* drow = dst + (int64_t)r * g.W;
+        const int trow = (HY + r) * WS + 2;  // tile word 1 = first interior word, column 2
+        for (int w = lane; w < words_out; w += 32)
+            drow[w] = kk_smem[trow + w] & (w == words_out - 1 ? last_mask : 0xFFFFFFFFu);
     }
 
     // ---- counters: warp reduce, block reduce, one atomic per CTA per counter
@@ -442,9 +440,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) pass_kernel(const PassPa
 
 int pass_smem_bytes(int T, int THI, int TWI) {
     const int H = THI + 6 * T, Wt = TWI + 2, WS = Wt + 2;
-    int tile_bytes = H * WS * 4;
-    tile_bytes = (tile_bytes + 15) / 16 * 16;
-    return tile_bytes + Wt * 8 + Wt * 4 + H * 4;
+    const int tile_words = (H * WS + 1) & ~1;
+    return 4 * (tile_words + 2 * Wt + Wt + H);
 }
 
 cudaError_t launch_pass(int T, const PassParams& P, int grid_y, int replicas, cudaStream_t stream) {

@@ -52,4 +52,4 @@ def test_version_and_errors_without_gpu(lib):
     assert b"sm_100a" in lib.kk_version()
     from paper_1309_4349_b200 import kk
     with pytest.raises(kk.KKError):
-        kk.Lattice(12, 8, 0.5, 0.5, 1)     # Lx % 8 != 0 -> argument error, before any CUDA call
+        kk.Lattice(10, 8, 0.5, 0.5, 1)     # Lx % 4 != 0 -> argument error, before any CUDA call

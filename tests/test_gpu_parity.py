@@ -128,6 +128,7 @@ def test_iters_per_pass_all_equal_oracle(T):
 
 
 @pytest.mark.parametrize("Lx,Ly,env", [
+    (4, 4, None), (12, 8, None), (20, 12, None), (36, 40, {"KK_TWI": 1, "KK_THI": 8}),
     (8, 4, None), (16, 8, None), (40, 12, None), (72, 20, None),
     (200, 52, {"KK_TWI": 2, "KK_THI": 16}),      # many tiles, ragged last tile (W=7)
     (1000, 44, {"KK_TWI": 5, "KK_THI": 12}),     # Lx % 32 = 8, ragged in x and y
