@@ -11,6 +11,9 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "../../include/kk.h"
 #include "kk_internal.cuh"
 
@@ -20,7 +23,8 @@ static std::atomic<long long> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 int pass_smem_bytes(int T, int THI, int TWI);
-cudaError_t launch_pass(int T, const PassParams& P, int grid_y, int replicas, cudaStream_t stream);
+cudaError_t launch_pass(int T, const PassParams& P, const CUtensorMap& tmap, int grid_y, int replicas,
+                        cudaStream_t stream);
 cudaError_t launch_observe(const ObsParams& P, cudaStream_t s);
 cudaError_t launch_init_block(uint32_t* lat, const Geom& g, int64_t replicas, int64_t nA, cudaStream_t s);
 cudaError_t launch_select_hist(const Geom& g, int64_t rep0, int64_t nrep, int level, const uint32_t* prefix,
@@ -63,6 +67,8 @@ struct kk_lattice {
     int64_t sweep = 0;
     int j = 0;
     int THI = 0, TWI = 0, tiles_x = 0, bands = 0, b_lo = 0, b_hi = 0;
+    int use_tma = 0, box_h = 0;
+    CUtensorMap tmap[2];              // TMA descriptors of buf[0], buf[1]
     // cluster analysis workspace (lazy)
     uint32_t* edges = nullptr;
     uint32_t* node_size = nullptr;
@@ -168,7 +174,41 @@ PassParams make_pass_params(kk_lattice* h, const uint32_t* ht, const uint32_t* h
         P.rk[10 + r] = P.key1 + (uint32_t)r * 0xBB67AE85u;
     }
     for (int k = 0; k < 7; ++k) P.thr[k] = h->thr[k];
+    P.use_tma = h->use_tma;
+    P.box_h = h->box_h;
+    P.vec_wb = (h->g.tail == 0 && h->g.W % 4 == 0 && h->TWI % 4 == 0) ? 1 : 0;
     return P;
+}
+
+// TMA descriptors for the two lattice buffers: a 3D uint32 tensor
+// (W words, rows, replicas) read in boxes of (TWI + 8) words x box_h rows.
+void make_tensor_maps(kk_lattice* h) {
+    h->use_tma = 0;
+    const int WS = h->TWI + 8, H = h->THI + 6 * h->T;
+    // Opt-in (KK_TMA=1): on the round-1 B200 image the in-kernel TMA staging
+    // raised "illegal instruction" although the same descriptor and PTX work in
+    // tools/tma_probe.cu; root cause open, so the default staging is
+    // the coalesced LDG path.
+    if (h->g.tail != 0 || h->g.W % 4 != 0 || WS % 4 != 0 || WS > 256 || !env_int("KK_TMA", 0)) return;
+    PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode), cudaEnableDefault,
+                                &q) != cudaSuccess || q != cudaDriverEntryPointSuccess || !encode) {
+        cudaGetLastError();
+        return;
+    }
+    h->box_h = std::min(256, H);
+    const cuuint64_t dims[3] = {(cuuint64_t)h->g.W, (cuuint64_t)h->g.rows, (cuuint64_t)h->R};
+    const cuuint64_t strides[2] = {(cuuint64_t)h->g.W * 4, (cuuint64_t)h->g.rows * h->g.W * 4};
+    const cuuint32_t box[3] = {(cuuint32_t)WS, (cuuint32_t)h->box_h, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    for (int b = 0; b < 2; ++b) {
+        CUresult r = encode(&h->tmap[b], CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, h->buf[b], dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return;
+    }
+    h->use_tma = 1;
 }
 
 int run_pass(kk_lattice* h, int region, const uint32_t* ht, const uint32_t* hb, cudaStream_t s) {
@@ -186,7 +226,7 @@ int run_pass(kk_lattice* h, int region, const uint32_t* ht, const uint32_t* hb, 
     } else {
         return fail(KK_ERR_ARG, "kk_pass: bad region");
     }
-    KK_CUDA(launch_pass(h->T, P, grid_y, (int)h->R, s));  // grid.z = replica (R <= 65535)
+    KK_CUDA(launch_pass(h->T, P, h->tmap[h->cur], grid_y, (int)h->R, s));  // grid.z = replica (R <= 65535)
     return KK_OK;
 }
 
@@ -399,6 +439,7 @@ int kk_create_ex(kk_handle* out, const kk_config* c) {
         delete h;
         return fail(KK_ERR_NOMEM, "device allocation failed");
     }
+    make_tensor_maps(h);
     cudaStream_t s = nullptr;
     int rc = KK_OK;
     if (cudaMemsetAsync(h->buf[0], 0, words * 4, s) || cudaMemsetAsync(h->buf[1], 0, words * 4, s) ||

@@ -72,7 +72,11 @@ __device__ __forceinline__ const uint32_t* row_source(const Geom& g, const uint3
                                                       const uint32_t* halo_top,
                                                       const uint32_t* halo_bot, int hy,
                                                       int64_t y) {
-    if (g.periodic) return lat + wrap_mod(y, g.rows) * g.W;
+    if (g.periodic) {
+        int64_t yy = y < 0 ? y + g.rows : (y >= g.rows ? y - g.rows : y);  // one wrap (common case)
+        if (yy < 0 || yy >= g.rows) yy = wrap_mod(y, g.rows);              // tiny lattices
+        return lat + yy * g.W;
+    }
     if (y >= 0 && y < g.rows) return lat + y * g.W;
     if (y < 0 && y >= -hy && halo_top) return halo_top + (y + hy) * g.W;
     if (y >= g.rows && y < g.rows + hy && halo_bot) return halo_bot + (y - g.rows) * g.W;
@@ -123,6 +127,9 @@ struct PassParams {
     uint32_t key0, key1;
     uint32_t rk[20];           // Philox round keys: key0 + r*W0 (r<10), key1 + r*W1
     uint32_t thr[7];           // accept iff u32 <= thr[v+3] (R5)
+    int32_t use_tma;           // interior tiles staged by cp.async.bulk.tensor (tensor map = src)
+    int32_t box_h;             // rows per TMA box
+    int32_t vec_wb;            // write-back with 16-byte vectors (W % 4 == 0, TWI % 4 == 0, no tail)
 };
 
 struct ObsParams {

@@ -23,6 +23,8 @@
 // (north_star part 4; R5).  Flips are XOR masks applied with shared-memory
 // atomics (bits of different centres are disjoint, so the XORs commute and
 // the result does not depend on thread scheduling).
+#include <cuda.h>  // CUtensorMap (TMA descriptor type only; no driver calls here)
+
 #include "kk_internal.cuh"
 
 namespace kk {
@@ -110,17 +112,58 @@ __device__ __forceinline__ void acc_flush(Acc& a) {
 }
 
 
-// Dynamic shared memory: the tile (H rows x WS words; columns 0 and WS-1 are
-// zero guards) at offset 0, then the per-pass tables.  Addressed through the
-// shared-space symbol so every access compiles to LDS/ATOMS with no generic
-// pointer conversion.
-extern __shared__ uint32_t kk_smem[];
-__shared__ uint2 kk_thr2[256];  // thresholds of the two nibbles of a byte of idx
+// Dynamic shared memory: the tile (H rows x WS = Wt + 6 words) at offset 0,
+// then the per-pass tables.  Tile word w (0..Wt-1; 0 and Wt-1 are the halo
+// words) lives in column w + kCol0; the three columns on each side are guards
+// whose contents never reach the interior (light cone, R8).  With
+// TWI = 64 the row pitch is 288 bytes and the interior starts 16 bytes into
+// the row, so rows can be filled by TMA boxes and written back with 16-byte
+// vectors.  Addressed through the shared-space symbol so every access is a
+// plain LDS/ATOMS.
+constexpr int kCol0 = 3;
+extern __shared__ __align__(128) uint32_t kk_smem[];
+// No static __shared__ variables in the pass kernel: the dynamic region then
+// starts at the beginning of the CTA's shared window, which keeps the tile
+// 128-byte aligned for the TMA destination.
+
+// ---- TMA (cp.async.bulk.tensor) staging of interior tiles ----------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "LAB_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE;\n\t"
+        "bra LAB_WAIT;\n"
+        "DONE:\n\t}" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint64_t* bar, int x, int y, int z) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
 
 struct Tabs {
     int mt_off;                // uint2 [Wt]: (global x of bit 0, word holds one aligned octet of centres)
     int wm_off;                // uint32 [Wt]: owned bits of the word (0 for halo words)
     int rl_off;                // uint32 [H]: centre-row index l | owned-row flag << 31
+    int th_off;                // uint2 [256]: thresholds of the two nibbles of a byte of idx
     uint32_t Lx;
     int WS;
 };
@@ -167,7 +210,7 @@ __device__ __forceinline__ void process_item(const Tabs& S, int r, int w, uint32
     }
 
     // ---- neighbourhood: rows r-2..r+2, columns w..w+2 (w+1 is the word itself)
-    const int t0 = (r - 2) * S.WS + w;
+    const int t0 = (r - 2) * S.WS + w + kCol0 - 1;
     uint32_t L[5], M[5], R[5];
 #pragma unroll
     for (int k = 0; k < 5; ++k) {
@@ -222,7 +265,7 @@ __device__ __forceinline__ void process_item(const Tabs& S, int r, int w, uint32
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
         const uint32_t byte = __byte_perm(idx, 0u, 0x4440u | (uint32_t)p);
-        const uint2 t2 = kk_thr2[byte];
+        const uint2 t2 = reinterpret_cast<const uint2*>(kk_smem + S.th_off)[byte];
         accb += (u[2 * p] <= t2.x ? 1u : 0u) << (8 * p);
         accb += (u[2 * p + 1] <= t2.y ? 1u : 0u) << (8 * p + 4);
     }
@@ -242,7 +285,7 @@ __device__ __forceinline__ void process_item(const Tabs& S, int r, int w, uint32
     const uint32_t Fr = (AN << KX) | (R0 << (KX + 1)) | ((R3 << KX) >> 1);
     const uint32_t Fu = ((up ^ U1) << KX) | (U1 << (KX + 1));
     const uint32_t Fd = ((dn ^ D4) << KX) | ((D4 << KX) >> 1);
-    const int ro = r * S.WS + w + 1;
+    const int ro = r * S.WS + w + kCol0;
     if (Fr) atomicXor(&kk_smem[ro], Fr);
     if (Fu) atomicXor(&kk_smem[ro + S.WS], Fu);
     if (Fd) atomicXor(&kk_smem[ro - S.WS], Fd);
@@ -291,15 +334,15 @@ __device__ __forceinline__ void run_iteration(const Tabs& S, int Wt, int r_first
 }
 
 template <int T>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) pass_kernel(const PassParams P) {
-    __shared__ unsigned long long red[4][kThreads / 32];
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+    pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassParams P) {
     constexpr int HY = 3 * T;
     const int rep = blockIdx.z;
     const int band = (int)blockIdx.y < P.nA ? P.bA + (int)blockIdx.y : P.bB + ((int)blockIdx.y - P.nA);
     const int64_t Y0 = (int64_t)band * P.THI;
     const int64_t X0 = (int64_t)blockIdx.x * P.TWI * 32;
     const int Wt = P.TWI + 2;
-    const int WS = Wt + 2;
+    const int WS = Wt + 6;
     const int H = P.THI + 2 * HY;
     const Geom& g = P.g;
     const uint32_t* src = P.src + rep * g.rep_words;
@@ -312,9 +355,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) pass_kernel(const PassPa
     S.mt_off = (H * WS + 1) & ~1;     // uint2 table, 8-byte aligned
     S.wm_off = S.mt_off + 2 * Wt;
     S.rl_off = S.wm_off + Wt;
+    S.th_off = (S.rl_off + H + 1) & ~1;
+    unsigned long long* red = reinterpret_cast<unsigned long long*>(kk_smem + S.th_off + 512);  // [4][warps]
+    uint64_t* tma_bar = reinterpret_cast<uint64_t*>(red + 4 * (kThreads / 32));
+    uint2* thr2 = reinterpret_cast<uint2*>(kk_smem + S.th_off);
     uint2* mtab = reinterpret_cast<uint2*>(kk_smem + S.mt_off);
     for (int b = threadIdx.x; b < 256; b += kThreads)
-        kk_thr2[b] = make_uint2(P.thr[min(b & 15, 6)], P.thr[min(b >> 4, 6)]);
+        thr2[b] = make_uint2(P.thr[min(b & 15, 6)], P.thr[min(b >> 4, 6)]);
 
     // ---- per-pass tables
     for (int w = threadIdx.x; w < Wt; w += kThreads) {
@@ -335,21 +382,39 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) pass_kernel(const PassPa
         kk_smem[S.rl_off + r] = (uint32_t)(yg >> 2) | (owned ? 0x80000000u : 0u);
     }
 
-    // ---- stage tile + halo (coalesced 32-bit loads, periodic in x)
+    // ---- stage tile + halo
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t gw0 = X0 / 32 - 1;
+    // TMA: a tile whose rows and words all lie inside this handle's lattice is
+    // copied by a few 3D boxes (WS words x box_h rows x 1 replica) starting at
+    // word gw0 - (kCol0 - 1); guard columns receive real (or zero OOB) data.
+    const bool tma_tile = P.use_tma && Y0 - HY >= 0 && Y0 - HY + H <= g.rows && gw0 >= 0 && gw0 + Wt <= g.W;
+    if (tma_tile) {
+        if (threadIdx.x == 0) mbar_init(tma_bar, 1);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int nbox = (H + P.box_h - 1) / P.box_h;
+            mbar_expect_tx(tma_bar, (uint32_t)(nbox * P.box_h * WS * 4));
+            for (int b = 0; b < nbox; ++b) {
+                const int y0 = min(b * P.box_h, H - P.box_h);  // last box may overlap the previous one
+                tma_load_3d(smem_u32(kk_smem + y0 * WS), &tmap, tma_bar, (int)(gw0 - (kCol0 - 1)),
+                            (int)(Y0 - HY + y0), rep);
+            }
+        }
+        mbar_wait(tma_bar, 0);
+    }
     // no x wrap and whole words: plain contiguous row copies
     const bool contiguous = g.tail == 0 && gw0 >= 0 && gw0 + Wt <= g.W;
-    for (int r = warp; r < H; r += kThreads / 32) {
+    for (int r = warp; r < (tma_tile ? 0 : H); r += kThreads / 32) {
         const uint32_t* row = row_source(g, src, htop, hbot, HY, Y0 - HY + r);
-        const int trow = r * WS;
-        if (lane == 0) {
-            kk_smem[trow] = 0u;
-            kk_smem[trow + WS - 1] = 0u;
+        const int trow = r * WS + kCol0;
+        if (lane < kCol0) {
+            kk_smem[trow - 1 - lane] = 0u;
+            kk_smem[trow + Wt + lane] = 0u;
         }
         if (contiguous && row) {
             const uint32_t* rp = row + gw0;
-            for (int w = lane; w < Wt; w += 32) kk_smem[trow + 1 + w] = rp[w];
+            for (int w = lane; w < Wt; w += 32) kk_smem[trow + w] = rp[w];
             continue;
         }
         for (int w = lane; w < Wt; w += 32) {
@@ -367,7 +432,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) pass_kernel(const PassPa
                     v = get32(row, p, g);
                 }
             }
-            kk_smem[trow + 1 + w] = v;
+            kk_smem[trow + w] = v;
         }
     }
     __syncthreads();
@@ -404,11 +469,21 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) pass_kernel(const PassPa
     const int words_out = (int)min64(P.TWI, g.W - X0 / 32);
     uint32_t* dst = P.dst + rep * g.rep_words + Y0 * g.W + X0 / 32;
     const uint32_t last_mask = (X0 / 32 + words_out == g.W) ? word_mask(g, g.W - 1) : 0xFFFFFFFFu;
-    for (int r = warp; r < rows_out; r += kThreads / 32) {
-        uint32_t* drow = dst + (int64_t)r * g.W;
-        const int trow = (HY + r) * WS + 2;  // tile word 1 = first interior word, column 2
-        for (int w = lane; w < words_out; w += 32)
-            drow[w] = kk_smem[trow + w] & (w == words_out - 1 ? last_mask : 0xFFFFFFFFu);
+    if (P.vec_wb && words_out == P.TWI && last_mask == 0xFFFFFFFFu) {
+        // 16-byte vectors: P.TWI % 4 == 0, W % 4 == 0, interior column offset 16 B
+        const int vpr = P.TWI / 4;  // vectors per row
+        for (int i = threadIdx.x; i < rows_out * vpr; i += kThreads) {
+            const int r = i / vpr, v = i - r * vpr;
+            const uint4 val = *reinterpret_cast<const uint4*>(kk_smem + (HY + r) * WS + kCol0 + 1 + 4 * v);
+            *reinterpret_cast<uint4*>(dst + (int64_t)r * g.W + 4 * v) = val;
+        }
+    } else {
+        for (int r = warp; r < rows_out; r += kThreads / 32) {
+            uint32_t* drow = dst + (int64_t)r * g.W;
+            const int trow = (HY + r) * WS + kCol0 + 1;  // tile word 1 = first interior word
+            for (int w = lane; w < words_out; w += 32)
+                drow[w] = kk_smem[trow + w] & (w == words_out - 1 ? last_mask : 0xFFFFFFFFu);
+        }
     }
 
     // ---- counters: warp reduce, block reduce, one atomic per CTA per counter
@@ -423,15 +498,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) pass_kernel(const PassPa
         v3 += __shfl_xor_sync(0xFFFFFFFFu, v3, o);
     }
     if (lane == 0) {
-        red[0][warp] = v0;
-        red[1][warp] = v1;
-        red[2][warp] = v2;
-        red[3][warp] = (unsigned long long)v3;
+        red[0 * (kThreads / 32) + warp] = v0;
+        red[1 * (kThreads / 32) + warp] = v1;
+        red[2 * (kThreads / 32) + warp] = v2;
+        red[3 * (kThreads / 32) + warp] = (unsigned long long)v3;
     }
     __syncthreads();
     if (threadIdx.x < 4) {
         unsigned long long s = 0;
-        for (int k = 0; k < kThreads / 32; ++k) s += red[threadIdx.x][k];
+        for (int k = 0; k < kThreads / 32; ++k) s += red[threadIdx.x * (kThreads / 32) + k];
         if (s) atomicAdd(P.stats + rep * 4 + threadIdx.x, s);
     }
 }
@@ -439,12 +514,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) pass_kernel(const PassPa
 }  // namespace
 
 int pass_smem_bytes(int T, int THI, int TWI) {
-    const int H = THI + 6 * T, Wt = TWI + 2, WS = Wt + 2;
+    const int H = THI + 6 * T, Wt = TWI + 2, WS = Wt + 6;
     const int tile_words = (H * WS + 1) & ~1;
-    return 4 * (tile_words + 2 * Wt + Wt + H);
+    const int th_off = (tile_words + 2 * Wt + Wt + H + 1) & ~1;
+    return 4 * (th_off + 512 + 2 * 4 * (kThreads / 32) + 2);
 }
 
-cudaError_t launch_pass(int T, const PassParams& P, int grid_y, int replicas, cudaStream_t stream) {
+cudaError_t launch_pass(int T, const PassParams& P, const CUtensorMap& tmap, int grid_y, int replicas,
+                        cudaStream_t stream) {
     const int smem = pass_smem_bytes(T, P.THI, P.TWI);
     dim3 grid(P.tiles_x, grid_y, replicas);
     if (grid_y == 0) return cudaSuccess;
@@ -453,7 +530,7 @@ cudaError_t launch_pass(int T, const PassParams& P, int grid_y, int replicas, cu
     case TT:                                                                                           \
         e = cudaFuncSetAttribute(pass_kernel<TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
         if (e != cudaSuccess) return e;                                                                \
-        pass_kernel<TT><<<grid, kThreads, smem, stream>>>(P);                                          \
+        pass_kernel<TT><<<grid, kThreads, smem, stream>>>(tmap, P);                                          \
         break;
     switch (T) {
         KK_LAUNCH(1)
