@@ -31,7 +31,7 @@ constexpr int kTW = 8;                     // tile words per row (256 sites)
 constexpr int kTX = 32 * kTW;              // tile sites per row
 constexpr int kSites = kTR * kTX;          // 8192
 constexpr int kEdge = 2 * kTX + 2 * kTR;   // edge entries per tile
-constexpr int kThreads = 512;
+constexpr int kThreads = 256;  // one thread per tile word in the per-word phases
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 // 32-bit labels in shared memory: sub-word CAS is emulated by a CAS loop on the
 // containing word, which races with the plain 16-bit stores of path halving.
@@ -134,8 +134,9 @@ __global__ void __launch_bounds__(kThreads) ccl_tile_kernel(const CclParams P) {
     uint32_t* S = tb + kTR * kTW;        // [kTR*kTW] run-start bits
     uint32_t* touch = S + kTR * kTW;     // [kSites/32] edge-touch flag per root
     uint32_t* lab = touch + kSites / 32; // [kSites] parent of each run start
-    uint32_t* cnt = lab + kSites;        // [kSites] size per root, then local node index
-    uint16_t* node_s = reinterpret_cast<uint16_t*>(cnt + kSites);  // [kEdge]
+    uint32_t* cnt32 = lab + kSites;      // [kSites/2] 16-bit size per root (two per word), then node index
+    uint16_t* cnt = reinterpret_cast<uint16_t*>(cnt32);
+    uint16_t* node_s = reinterpret_cast<uint16_t*>(cnt32 + kSites / 2);  // [kEdge]
     __shared__ unsigned int n_nodes, node_base;
 
     const Geom& g = P.g;
@@ -205,7 +206,7 @@ __global__ void __launch_bounds__(kThreads) ccl_tile_kernel(const CclParams P) {
             const int x0 = 32 * w + __ffs(seg) - 1;
             const int x1 = 32 * w + 31 - __clz(seg);
             const uint32_t root = root_of(lab, run_start(S, r, x0));
-            atomicAdd(&cnt[root], (uint32_t)__popc(seg));
+            atomicAdd(&cnt32[root >> 1], (uint32_t)__popc(seg) << (16 * (root & 1)));
             if (edge_row || x0 == 0 || x1 == w_tile - 1) atomicOr(&touch[root >> 5], 1u << (root & 31));
         }
     }
@@ -216,7 +217,7 @@ __global__ void __launch_bounds__(kThreads) ccl_tile_kernel(const CclParams P) {
         for (uint32_t m = S[i]; m; m &= m - 1) {
             const uint32_t s0 = base + __ffs(m) - 1;
             if (lab[s0] != s0) continue;
-            const uint32_t sz = cnt[s0];
+            const uint32_t sz = cnt[s0];  // <= kSites fits 16 bits
             if ((touch[s0 >> 5] >> (s0 & 31)) & 1u) {
                 const unsigned int k = atomicAdd(&n_nodes, 1u);
                 node_s[k] = (uint16_t)sz;
@@ -444,7 +445,7 @@ cudaError_t launch_ccl(const uint32_t* lat, const Geom& g, int64_t replicas, int
     P.node_cap = ccl_node_cap(g, replicas);
     cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(unsigned int), s);
     if (e != cudaSuccess) return e;
-    const int smem = 4 * (2 * kTR * kTW + kSites / 32 + 2 * kSites) + 2 * kEdge;
+    const int smem = 4 * (2 * kTR * kTW + kSites / 32 + kSites + kSites / 2) + 2 * kEdge;
     e = cudaFuncSetAttribute(ccl_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     ccl_tile_kernel<<<dim3(P.tiles_x, P.tiles_y, (unsigned)replicas), kThreads, smem, s>>>(P);
