@@ -286,9 +286,10 @@ __device__ __forceinline__ void process_item(const Tabs& S, int r, int w, uint32
     const uint32_t Fu = ((up ^ U1) << KX) | (U1 << (KX + 1));
     const uint32_t Fd = ((dn ^ D4) << KX) | ((D4 << KX) >> 1);
     const int ro = r * S.WS + w + kCol0;
-    if (Fr) atomicXor(&kk_smem[ro], Fr);
-    if (Fu) atomicXor(&kk_smem[ro + S.WS], Fu);
-    if (Fd) atomicXor(&kk_smem[ro - S.WS], Fd);
+    // unconditional (XOR with 0 is a no-op): no per-item branch/reconvergence
+    atomicXor(&kk_smem[ro], Fr);
+    atomicXor(&kk_smem[ro + S.WS], Fu);
+    atomicXor(&kk_smem[ro - S.WS], Fd);
     if constexpr (KX == 3) {  // centre at bit 31 moving right: partner in the next word
         if (R0 >> 28) atomicXor(&kk_smem[ro + 1], 1u);
         if (U1 >> 28) atomicXor(&kk_smem[ro + S.WS + 1], 1u);
