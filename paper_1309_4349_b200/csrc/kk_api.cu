@@ -23,6 +23,8 @@ static std::atomic<long long> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 int pass_smem_bytes(int T, int THI, int TWI);
+int resident_smem_bytes(const Geom& g);
+cudaError_t launch_resident(const ResParams& P, int64_t replicas, cudaStream_t stream);
 cudaError_t launch_pass(int T, const PassParams& P, const CUtensorMap& tmap, int grid_y, int replicas,
                         cudaStream_t stream);
 cudaError_t launch_observe(const ObsParams& P, cudaStream_t s);
@@ -68,6 +70,7 @@ struct kk_lattice {
     int j = 0;
     int THI = 0, TWI = 0, tiles_x = 0, bands = 0, b_lo = 0, b_hi = 0;
     int use_tma = 0, box_h = 0;
+    int resident = 0;                 // kk_sweep runs the resident kernel (whole replica in shared memory)
     CUtensorMap tmap[2];              // TMA descriptors of buf[0], buf[1]
     // cluster analysis workspace (lazy)
     uint32_t* edges = nullptr;
@@ -425,6 +428,15 @@ int kk_create_ex(kk_handle* out, const kk_config* c) {
     h->hy = 3 * T;
     make_thresholds(h->omega, h->thr);
     choose_tiles(h);
+    {
+        // resident kernel: one CTA per replica, all sweeps of a kk_sweep call in
+        // one launch.  Auto (KK_RESIDENT=1, default) when the tile kernel would
+        // not spread a replica over more than two CTAs anyway; 2 = whenever the
+        // replica fits; 0 = never.
+        const int mode = env_int("KK_RESIDENT", 1);
+        const int64_t tile_ctas = (int64_t)h->tiles_x * h->bands;
+        h->resident = resident_smem_bytes(h->g) > 0 && (mode == 2 || (mode == 1 && tile_ctas <= 2)) ? 1 : 0;
+    }
     if (pass_smem_bytes(T, h->THI, h->TWI) > 227 * 1024) {
         delete h;
         return fail(KK_ERR_ARG, "tile too large for shared memory (KK_THI/KK_TWI)");
@@ -512,6 +524,25 @@ int kk_sweep(kk_handle h, int64_t n, void* stream) {
     KK_CHECK_HANDLE(h);
     if (!h->g.periodic) return fail(KK_ERR_STATE, "kk_sweep: slab handle (use kk_pass)");
     if (n < 0) return fail(KK_ERR_ARG, "n must be >= 0");
+    if (h->resident && n > 0) {
+        ResParams P{};
+        P.src = h->buf[h->cur];
+        P.dst = h->buf[h->cur ^ 1];
+        P.stats = h->stats;
+        P.g = h->g;
+        P.sweep0 = (uint32_t)h->sweep;
+        P.j0 = h->j;
+        P.n_iters = 16 * n;
+        const PassParams Q = make_pass_params(h, nullptr, nullptr);
+        P.key0 = Q.key0;
+        P.key1 = Q.key1;
+        for (int k = 0; k < 20; ++k) P.rk[k] = Q.rk[k];
+        for (int k = 0; k < 7; ++k) P.thr[k] = Q.thr[k];
+        KK_CUDA(launch_resident(P, h->R, S(stream)));
+        h->cur ^= 1;
+        h->sweep += n;
+        return KK_OK;
+    }
     const int64_t passes = n * (16 / h->T);
     for (int64_t p = 0; p < passes; ++p) {
         int rc = run_pass(h, KK_REGION_ALL, nullptr, nullptr, S(stream));

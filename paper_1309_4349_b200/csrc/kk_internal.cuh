@@ -132,6 +132,21 @@ struct PassParams {
     int32_t vec_wb;            // write-back with 16-byte vectors (W % 4 == 0, TWI % 4 == 0, no tail)
 };
 
+// Resident kernel (kk_pass.cu): one CTA holds one whole replica in shared
+// memory for n_iters iterations (non-slab handles whose replica fits).
+struct ResParams {
+    const uint32_t* src;       // current lattice, replica 0
+    uint32_t* dst;             // next lattice, replica 0
+    unsigned long long* stats; // [replicas][4]
+    Geom g;
+    uint32_t sweep0;           // sweep of the first iteration
+    int32_t j0;                // its index within the sweep
+    int64_t n_iters;           // iterations to run
+    uint32_t key0, key1;
+    uint32_t rk[20];
+    uint32_t thr[7];
+};
+
 struct ObsParams {
     const uint32_t* lat;
     const uint32_t* halo_bot;  // slab: next slab's first rows, replica stride halo_stride, or nullptr

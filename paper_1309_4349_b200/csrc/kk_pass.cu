@@ -166,10 +166,15 @@ struct Tabs {
     int th_off;                // uint2 [256]: thresholds of the two nibbles of a byte of idx
     uint32_t Lx;
     int WS;
+    int rW, rTail, rRows;      // resident kernel: lattice words, Lx % 32, rows (tile kernel: unused)
 };
 
 // One work item: the 8 centres of tile word w (column w+1) in row r.
-template <int KX>
+// RES = the resident kernel's layout (whole replica in shared memory, wrapped
+// copies in guard rows/words): only owned centres flip, and a flip that lands
+// on a copy is applied to the true site instead (copies are rebuilt after
+// every iteration).
+template <int KX, bool RES = false>
 __device__ __forceinline__ void process_item(const Tabs& S, int r, int w, uint32_t sweep, uint32_t c3,
                                              const uint32_t* rk, Acc& acc) {
     const uint32_t rl = kk_smem[S.rl_off + r];
@@ -269,7 +274,12 @@ __device__ __forceinline__ void process_item(const Tabs& S, int r, int w, uint32
         accb += (u[2 * p] <= t2.x ? 1u : 0u) << (8 * p);
         accb += (u[2 * p + 1] <= t2.y ? 1u : 0u) << (8 * p + 4);
     }
-    const uint32_t AN = accb & Dsel;
+    uint32_t AN = accb & Dsel;
+    uint32_t wm = 0;
+    if constexpr (RES) {
+        wm = (kk_smem[S.wm_off + w] >> KX) & kNib;
+        AN &= wm;
+    }
 
     // ---- flips (XOR masks).  Directions by row: d=0 (+1,0) and d=3 (-1,0)
     // stay in row r, d=1 (+1,+1) and d=2 (0,+1) go to r+1, d=4 (-1,-1) and
@@ -282,25 +292,55 @@ __device__ __forceinline__ void process_item(const Tabs& S, int r, int w, uint32
     const uint32_t D4 = dn & ~b0;               // (-1,-1)
     const uint32_t R0 = same & ~b0;             // (+1, 0)
     const uint32_t R3 = same & b0;              // (-1, 0)
-    const uint32_t Fr = (AN << KX) | (R0 << (KX + 1)) | ((R3 << KX) >> 1);
-    const uint32_t Fu = ((up ^ U1) << KX) | (U1 << (KX + 1));
-    const uint32_t Fd = ((dn ^ D4) << KX) | ((D4 << KX) >> 1);
+    uint32_t Fr = (AN << KX) | (R0 << (KX + 1)) | ((R3 << KX) >> 1);
+    uint32_t Fu = ((up ^ U1) << KX) | (U1 << (KX + 1));
+    uint32_t Fd = ((dn ^ D4) << KX) | ((D4 << KX) >> 1);
     const int ro = r * S.WS + w + kCol0;
+    int ro_u = ro + S.WS, ro_d = ro - S.WS;
+    int nxt = 1, prv = -1;                    // word offsets of the right / left carries
+    uint32_t prv_bit = 0x80000000u;
+    if constexpr (RES) {
+        // periodic rows: real rows are 2..rRows+1
+        if (r == S.rRows + 1) ro_u -= S.rRows * S.WS;
+        if (r == 2) ro_d += S.rRows * S.WS;
+        if (w == S.rW) {
+            if (S.rTail) {  // bits >= Lx % 32 of the last word are copies of x = 0.. (tile word 1)
+                const uint32_t ov = 0xFFFFFFFFu << S.rTail;
+                const int back = S.rW - 1;
+                atomicXor(&kk_smem[ro - back], (Fr & ov) >> S.rTail);
+                atomicXor(&kk_smem[ro_u - back], (Fu & ov) >> S.rTail);
+                atomicXor(&kk_smem[ro_d - back], (Fd & ov) >> S.rTail);
+                Fr &= ~ov;
+                Fu &= ~ov;
+                Fd &= ~ov;
+            }
+            nxt = 1 - S.rW;
+        }
+        if (w == 1) {
+            prv = S.rW - 1;
+            prv_bit = 1u << ((S.rTail ? S.rTail : 32) - 1);
+        }
+    }
     // unconditional (XOR with 0 is a no-op): no per-item branch/reconvergence
     atomicXor(&kk_smem[ro], Fr);
-    atomicXor(&kk_smem[ro + S.WS], Fu);
-    atomicXor(&kk_smem[ro - S.WS], Fd);
+    atomicXor(&kk_smem[ro_u], Fu);
+    atomicXor(&kk_smem[ro_d], Fd);
     if constexpr (KX == 3) {  // centre at bit 31 moving right: partner in the next word
-        if (R0 >> 28) atomicXor(&kk_smem[ro + 1], 1u);
-        if (U1 >> 28) atomicXor(&kk_smem[ro + S.WS + 1], 1u);
+        if (R0 >> 28) atomicXor(&kk_smem[ro + nxt], 1u);
+        if (U1 >> 28) atomicXor(&kk_smem[ro_u + nxt], 1u);
     }
     if constexpr (KX == 0) {  // centre at bit 0 moving left: partner in the previous word
-        if (R3 & 1u) atomicXor(&kk_smem[ro - 1], 0x80000000u);
-        if (D4 & 1u) atomicXor(&kk_smem[ro - S.WS - 1], 0x80000000u);
+        if (R3 & 1u) atomicXor(&kk_smem[ro + prv], prv_bit);
+        if (D4 & 1u) atomicXor(&kk_smem[ro_d + prv], prv_bit);
     }
 
     // ---- counters over owned centres (branch-free; in_mask = 0 for halo)
-    const uint32_t in_mask = (rl >> 31) ? ((kk_smem[S.wm_off + w] >> KX) & kNib) : 0u;
+    uint32_t in_mask;
+    if constexpr (RES) {
+        in_mask = wm;
+    } else {
+        in_mask = (rl >> 31) ? ((kk_smem[S.wm_off + w] >> KX) & kNib) : 0u;
+    }
     const uint32_t A = AN & in_mask;
     acc.attempted += __popc(in_mask);
     acc.trivial += __popc(in_mask & ~Dsel);
@@ -512,6 +552,197 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     }
 }
 
+
+// ---- resident kernel -----------------------------------------------------------
+// For replicas small enough to live in shared memory (the paper's 400 x 400,
+// configs[3]'s replica batch): one CTA per replica stages it once, runs all
+// n_iters iterations without touching HBM, and writes it back once.  There is
+// no halo to recompute: the periodic wrap is kept as COPIES — guard rows
+// 0,1 / rows+2,rows+3 and tile words 0 / W+1 (plus the unused high bits of a
+// partial last word) hold the wrapped neighbours and are rebuilt from the
+// real words after every iteration; flips that land on a copy are redirected
+// to the true site inside process_item<KX, true>.
+//
+// Shared layout: row r (0..rows+3; real rows 2..rows+1 = y 0..rows-1), tile
+// word w (0..W+1; real words 1..W = lattice words 0..W-1) at r*WS + kCol0 + w.
+
+// Tile word w (0..W+1) of the row whose tile word 0 is at `base`, computed
+// from the real words 1..W only (of the last one only its low `tail` bits).
+__device__ __forceinline__ uint32_t res_word(int base, int w, int W, int tail) {
+    if (tail == 0) {
+        const int k = w == 0 ? W : (w == W + 1 ? 1 : w);
+        return kk_smem[base + k];
+    }
+    if (w == 0)  // sites Lx-32 .. Lx-1
+        return (kk_smem[base + W - 1] >> tail) | (kk_smem[base + W] << (32 - tail));
+    if (w == W)  // sites 32(W-1) .. Lx-1, then x = 0 ..
+        return (kk_smem[base + W] & ((1u << tail) - 1u)) | (kk_smem[base + 1] << tail);
+    if (w == W + 1)  // sites 32W .. 32W+31 = x (32 - tail) ..
+        return (kk_smem[base + 1] >> (32 - tail)) | (kk_smem[base + 2] << tail);
+    return kk_smem[base + w];
+}
+
+__device__ __forceinline__ void res_refresh(const Tabs& S) {
+    const int W = S.rW, tail = S.rTail, rows = S.rRows, WS = S.WS;
+    const int nx = tail ? 3 : 2;  // rewritten words of a real row: 0, W+1 (and W)
+    const int n_real = rows * nx, total = n_real + 4 * (W + 2);
+    for (int i = threadIdx.x; i < total; i += kThreads) {
+        int dst_row, src_row, w;
+        if (i < n_real) {
+            const int a = i / nx, k = i - a * nx;
+            dst_row = src_row = 2 + a;
+            w = k == 0 ? 0 : (k == 1 ? W + 1 : W);
+        } else {
+            const int i2 = i - n_real, gi = i2 / (W + 2);
+            w = i2 - gi * (W + 2);
+            dst_row = gi < 2 ? gi : rows + gi;      // 0, 1, rows+2, rows+3
+            src_row = gi < 2 ? rows + gi : gi;      // rows, rows+1, 2, 3
+        }
+        // a concurrent rewrite of word W only changes its copy bits, which
+        // res_word never reads
+        kk_smem[dst_row * WS + kCol0 + w] = res_word(src_row * WS + kCol0, w, W, tail);
+    }
+}
+
+template <int KX>
+__device__ __forceinline__ void res_iteration(const Tabs& S, int r_first, uint32_t sweep, uint32_t c3,
+                                              const uint32_t* rk, Acc& acc) {
+    const int W = S.rW;
+    const int items = (S.rRows / 4) * W;
+    int a = threadIdx.x / W;
+    int w = threadIdx.x - a * W;
+    const int da = kThreads / W, dw = kThreads - da * W;
+    int since_flush = 0;
+    for (int it = threadIdx.x; it < items; it += kThreads) {
+        process_item<KX, true>(S, r_first + 4 * a, w + 1, sweep, c3, rk, acc);
+        if (++since_flush == 32) {
+            acc_flush(acc);
+            since_flush = 0;
+        }
+        a += da;
+        w += dw;
+        if (w >= W) {
+            w -= W;
+            ++a;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, kMinBlocks) resident_kernel(const ResParams P) {
+    const int rep = blockIdx.x;
+    const Geom& g = P.g;
+    const int W = g.W, tail = g.tail, rows = (int)g.rows;
+    const int H = rows + 4, Wt = W + 2, WS = Wt + kCol0;
+    Tabs S;
+    S.WS = WS;
+    S.Lx = (uint32_t)g.Lx;
+    S.rW = W;
+    S.rTail = tail;
+    S.rRows = rows;
+    S.mt_off = (H * WS + 1) & ~1;
+    S.wm_off = S.mt_off + 2 * Wt;
+    S.rl_off = S.wm_off + Wt;
+    S.th_off = (S.rl_off + H + 1) & ~1;
+    unsigned long long* red = reinterpret_cast<unsigned long long*>(kk_smem + S.th_off + 512);
+    uint2* thr2 = reinterpret_cast<uint2*>(kk_smem + S.th_off);
+    uint2* mtab = reinterpret_cast<uint2*>(kk_smem + S.mt_off);
+    for (int b = threadIdx.x; b < 256; b += kThreads)
+        thr2[b] = make_uint2(P.thr[min(b & 15, 6)], P.thr[min(b >> 4, 6)]);
+    for (int w = threadIdx.x; w < Wt; w += kThreads) {
+        // every real word starts an aligned octet (x = 32(w-1)); in a partial
+        // last word the centres past Lx are masked out of wm
+        mtab[w] = make_uint2(w >= 1 ? 32u * (uint32_t)(w - 1) : 0u, 1u);
+        uint32_t own = 0;
+        if (w >= 1 && w <= W) own = (w == W && tail) ? ((1u << tail) - 1u) : 0xFFFFFFFFu;
+        kk_smem[S.wm_off + w] = own;
+    }
+    for (int r = threadIdx.x; r < H; r += kThreads)
+        kk_smem[S.rl_off + r] = (r >= 2 && r < rows + 2) ? ((uint32_t)((r - 2) >> 2) | 0x80000000u) : 0u;
+    // stage the replica
+    const uint32_t* src = P.src + rep * g.rep_words;
+    for (int i = threadIdx.x; i < rows * W; i += kThreads) {
+        const int y = i / W, x = i - y * W;
+        kk_smem[(y + 2) * WS + kCol0 + 1 + x] = src[i];
+    }
+    __syncthreads();
+    res_refresh(S);
+    __syncthreads();
+
+    // per-warp 64-bit totals in shared memory (lane 0 of each warp adds its
+    // warp's 32-bit sums once per sweep)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0)
+        for (int k = 0; k < 4; ++k) red[k * (kThreads / 32) + warp] = 0ull;
+    Acc acc = {0u, 0u, 0u, 0u, 0u, 0ull};
+    uint32_t sweep = P.sweep0;
+    int j = P.j0;
+    int64_t left = P.n_iters;
+#pragma unroll 1
+    while (left > 0) {
+        const Words4 sched = philox10(0u, 0u, sweep, ((uint32_t)rep << 8) | kTagSchedule, P.key0, P.key1);
+        const int jend = (int)min64(16, j + left);
+        left -= jend - j;
+#pragma unroll 1
+        for (; j < jend; ++j) {
+            const uint32_t k = ((j < 8 ? sched.a : sched.b) >> (4 * (j & 7))) & 15u;
+            const int kx = (int)(k & 3u), ky = (int)(k >> 2);
+            const uint32_t c3 = ((uint32_t)rep << 8) | (uint32_t)j;
+            switch (kx) {
+                case 0: res_iteration<0>(S, 2 + ky, sweep, c3, P.rk, acc); break;
+                case 1: res_iteration<1>(S, 2 + ky, sweep, c3, P.rk, acc); break;
+                case 2: res_iteration<2>(S, 2 + ky, sweep, c3, P.rk, acc); break;
+                default: res_iteration<3>(S, 2 + ky, sweep, c3, P.rk, acc); break;
+            }
+            acc_flush(acc);
+            __syncthreads();
+            res_refresh(S);
+            __syncthreads();
+        }
+        if (j == 16) {
+            j = 0;
+            ++sweep;
+        }
+        // per-sweep sums fit 32 bits (a thread handles <= 28 items per iteration)
+        uint32_t c0 = acc.attempted, c1 = acc.trivial, c2 = acc.accepted, c3s = (uint32_t)acc.idx_sum;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            c0 += __shfl_xor_sync(0xFFFFFFFFu, c0, o);
+            c1 += __shfl_xor_sync(0xFFFFFFFFu, c1, o);
+            c2 += __shfl_xor_sync(0xFFFFFFFFu, c2, o);
+            c3s += __shfl_xor_sync(0xFFFFFFFFu, c3s, o);
+        }
+        if (lane == 0) {
+            red[0 * (kThreads / 32) + warp] += c0;
+            red[1 * (kThreads / 32) + warp] += c1;
+            red[2 * (kThreads / 32) + warp] += c2;
+            red[3 * (kThreads / 32) + warp] += c3s;
+        }
+        acc.attempted = acc.trivial = acc.accepted = 0u;
+        acc.idx_sum = 0ull;
+    }
+
+    // write back the real words
+    uint32_t* dst = P.dst + rep * g.rep_words;
+    const uint32_t last = tail ? ((1u << tail) - 1u) : 0xFFFFFFFFu;
+    for (int i = threadIdx.x; i < rows * W; i += kThreads) {
+        const int y = i / W, x = i - y * W;
+        const uint32_t v = kk_smem[(y + 2) * WS + kCol0 + 1 + x];
+        dst[i] = x == W - 1 ? (v & last) : v;
+    }
+
+    // dN_AB total = 2 (sum of idx - 3 per accepted centre)
+    if (lane == 0)
+        red[3 * (kThreads / 32) + warp] =
+            (unsigned long long)(2 * ((long long)red[3 * (kThreads / 32) + warp] -
+                                      3 * (long long)red[2 * (kThreads / 32) + warp]));
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        unsigned long long s = 0;
+        for (int k = 0; k < kThreads / 32; ++k) s += red[threadIdx.x * (kThreads / 32) + k];
+        if (s) atomicAdd(P.stats + rep * 4 + threadIdx.x, s);
+    }
+}
+
 }  // namespace
 
 int pass_smem_bytes(int T, int THI, int TWI) {
@@ -519,6 +750,26 @@ int pass_smem_bytes(int T, int THI, int TWI) {
     const int tile_words = (H * WS + 1) & ~1;
     const int th_off = (tile_words + 2 * Wt + Wt + H + 1) & ~1;
     return 4 * (th_off + 512 + 2 * 4 * (kThreads / 32) + 2);
+}
+
+// 0 if the replica does not fit (or the layout needs Lx >= 64, W >= 3 with a tail)
+int resident_smem_bytes(const Geom& g) {
+    if (g.Lx < 64 || (g.tail && g.W < 3) || !g.periodic) return 0;
+    const int64_t H = g.rows + 4, Wt = g.W + 2, WS = Wt + kCol0;
+    const int64_t tile_words = (H * WS + 1) & ~1;
+    const int64_t th_off = (tile_words + 2 * Wt + Wt + H + 1) & ~1;
+    const int64_t bytes = 4 * (th_off + 512 + 2 * 4 * (kThreads / 32));
+    return bytes <= 227 * 1024 ? (int)bytes : 0;
+}
+
+cudaError_t launch_resident(const ResParams& P, int64_t replicas, cudaStream_t stream) {
+    const int smem = resident_smem_bytes(P.g);
+    if (!smem) return cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(resident_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    resident_kernel<<<(unsigned)replicas, kThreads, smem, stream>>>(P);
+    count_launch();
+    return cudaGetLastError();
 }
 
 cudaError_t launch_pass(int T, const PassParams& P, const CUtensorMap& tmap, int grid_y, int replicas,

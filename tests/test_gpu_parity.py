@@ -124,7 +124,7 @@ def test_config0_64x64_1000_sweeps():
 
 @pytest.mark.parametrize("T", [1, 2, 4, 8])
 def test_iters_per_pass_all_equal_oracle(T):
-    _run_parity(96, 40, 0.5, 0.6, 77, 12, T=T)
+    _run_parity(96, 40, 0.5, 0.6, 77, 12, T=T, env={"KK_RESIDENT": 0})   # tile kernel
 
 
 @pytest.mark.parametrize("Lx,Ly,env", [
@@ -193,7 +193,7 @@ def test_cluster_histogram_large_clusters():
 def test_config1_400x400_paper_size():
     """BASELINE configs[1] shapes: 400x400 at 50:50 and 30:70 compositions."""
     for f, om in [(0.5, 0.6), (0.3, 1.0)]:
-        L, ref = _run_parity(400, 400, f, om, 400, 3)
+        L, ref = _run_parity(400, 400, f, om, 400, 3)   # resident kernel (default)
         assert L.cluster_histogram(1)[0] == O.cluster_histogram(ref[0], 1)
 
 

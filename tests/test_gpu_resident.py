@@ -1,0 +1,90 @@
+"""Parity of the resident kernel (whole replica in shared memory, periodic
+wrap kept as rebuilt copies; kk_pass.cu resident_kernel) with the oracle, and
+of the tile kernel on the same shapes — both must give the oracle's lattice,
+counters and N_AB bit for bit (north_star: "bit-exact agreement with the CPU
+oracle on every config").
+
+KK_RESIDENT=2 forces the resident kernel whenever the replica fits, 0 forces
+the tile kernel; the default (1) picks the resident kernel when the tile
+kernel would use <= 2 CTAs per replica.
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tests import inputs
+from tests.test_gpu_parity import _gpu, _lat, _run_parity  # noqa: F401  (fixture)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("Lx,Ly,R", [
+    (64, 4, 1),      # smallest resident shape: two lattice words, 4 rows
+    (64, 8, 2),
+    (68, 12, 1),     # tail of 4 bits, W = 3 (minimum with a tail)
+    (96, 16, 1),     # no tail, W = 3
+    (100, 20, 3),    # tail of 4 bits
+    (120, 8, 1),     # tail of 24 bits
+    (128, 32, 1),
+    (400, 40, 2),    # tail of 16 bits (the paper's width)
+    (1000, 44, 1),   # Lx % 32 = 8
+    (4096, 12, 1),   # wide and short
+])
+@pytest.mark.parametrize("mode", [2, 0])
+def test_resident_and_tile_paths_match_oracle(Lx, Ly, R, mode):
+    _run_parity(Lx, Ly, 0.5, 0.7, Lx * 7 + Ly, 5, R=R, env={"KK_RESIDENT": mode})
+
+
+@pytest.mark.parametrize("omega", [0.0, 0.6, -1.0, 5.0])
+def test_resident_omega(omega):
+    _run_parity(100, 28, 0.3, omega, 11, 8, env={"KK_RESIDENT": 2})
+
+
+def test_resident_arbitrary_start_stripes():
+    """Striped start (domain walls on the wrap seams) and a random start."""
+    stripes = np.stack([inputs.striped_lattice(72, 16)] * 2)
+    _run_parity(72, 16, 0.5, 1.0, 17, 20, R=2, start=stripes, env={"KK_RESIDENT": 2})
+    start = inputs.random_lattice(100, 24, 0.45, seed=9, replicas=2)
+    _run_parity(100, 24, 0.5, 0.8, 4242, 15, R=2, start=start, env={"KK_RESIDENT": 2})
+
+
+def test_resident_mid_sweep_start():
+    """kk_pass (tile kernel, T=4) leaves the handle at iteration j=4; kk_sweep
+    (resident kernel) must continue from (sweep 0, j=4); three more passes
+    finish sweep 2 — the whole run equals 3 oracle sweeps."""
+    from paper_1309_4349_b200 import kk
+    Lx, Ly, seed, om = 100, 20, 31337, 0.9
+    L = _lat(Lx, Ly, 0.5, om, seed, iters_per_pass=4, env={"KK_RESIDENT": 2})
+    ref = O.init_random(Lx, Ly, 0.5, seed)
+    L.run_pass(kk.REGION_ALL, None, None)
+    L.pass_commit()
+    L.sweep(2)
+    for _ in range(3):
+        L.run_pass(kk.REGION_ALL, None, None)
+        L.pass_commit()
+    assert L.sweep_index() == 3
+    ost = O.run(ref, om, seed, 3)
+    assert np.array_equal(L.get_lattice()[0], ref)
+    st = L.stats()[0]
+    assert list(st) == [ost["attempted"], ost["trivial"], ost["accepted"], ost["dnab_sum"]]
+
+
+def test_config3_replica_batch_sample():
+    """BASELINE configs[3] (1024 x 400x400 replicas, resident by default):
+    all replicas conserve composition and keep N_AB = N_AB(0) + sum dN; a
+    sample of replicas matches the oracle bit for bit after 2 sweeps."""
+    R, Lx, Ly, seed, om = 1024, 400, 400, 2024, 0.6
+    L = _lat(Lx, Ly, 0.5, om, seed, replicas=R)
+    nab0 = L.energy()[0]
+    L.sweep(2)
+    st = L.stats()
+    nab1 = L.energy()[0]
+    assert (L.composition() == O.count_a_for(Lx * Ly, 0.5)).all()
+    assert np.array_equal(nab1 - nab0, st[:, 3])
+    assert (st[:, 0] == 2 * Lx * Ly).all()
+    got = L.get_lattice()
+    for r in [0, 1, 517, 1023]:
+        ref = O.init_random(Lx, Ly, 0.5, seed, replica=r)
+        ost = O.run(ref, om, seed, 2, replica=r)
+        assert np.array_equal(got[r], ref), r
+        assert list(st[r]) == [ost["attempted"], ost["trivial"], ost["accepted"], ost["dnab_sum"]]
