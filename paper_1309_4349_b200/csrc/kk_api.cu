@@ -136,9 +136,16 @@ void make_thresholds(double omega, uint32_t thr[7]) {
     }
 }
 
-void choose_tiles(kk_lattice* h) {
-    const int twi_t = std::max(1, env_int("KK_TWI", 64));
-    const int thi_t = std::max(4, env_int("KK_THI", 320));
+// Tile shape of the pass kernel.  KK_TWI / KK_THI force targets; otherwise a
+// small cost model picks the shape: per-CTA work ~ items over the T
+// iterations (interior + shrinking light cone, R8) + staging + a fixed cost
+// per CTA and per iteration (fitted to tools/tile_choice.py timings: within
+// ~3% over 19 shapes from 1024^2 to 65536^2), two CTAs share
+// an SM (smem <= 113 KB each), and an SM's time is its CTA count x the
+// per-CTA time (a CTA alone on an SM runs ~1.7x faster than a shared one).
+// Large lattices get 64-word x ~320-row tiles; mid-size lattices (4096^2)
+// get small tiles so that every SM has work.
+void set_tiles(kk_lattice* h, int twi_t, int thi_t) {
     const int64_t W = h->g.W, rows = h->g.rows;
     const int64_t nx = (W + twi_t - 1) / twi_t;
     h->TWI = (int)((W + nx - 1) / nx);
@@ -148,6 +155,39 @@ void choose_tiles(kk_lattice* h) {
     thi = (thi + 3) / 4 * 4;
     h->THI = (int)thi;
     h->bands = (int)((rows + thi - 1) / thi);
+}
+
+void choose_tiles(kk_lattice* h) {
+    const int twi_env = env_int("KK_TWI", 0), thi_env = env_int("KK_THI", 0);
+    if (twi_env > 0 || thi_env > 0) {
+        set_tiles(h, std::max(1, twi_env > 0 ? twi_env : 64), std::max(4, thi_env > 0 ? thi_env : 320));
+    } else {
+        int nsm = 148;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device);
+        if (nsm <= 0) nsm = 148;
+        const int T = h->T;
+        double best = 1e300;
+        int bt = 64, bh = 320;
+        for (int twi_t : {8, 16, 32, 64}) {
+            for (int thi_t = 8; thi_t <= 512; thi_t += 4) {
+                set_tiles(h, twi_t, thi_t);
+                if (pass_smem_bytes(T, h->THI, h->TWI) > 113 * 1024) continue;
+                const double items = (double)(h->TWI + 6) * (h->THI + 3 * T - 1) * T / 4.0;
+                const double stage = (double)(h->TWI + 16) * (h->THI + 6 * T) / 8.0;
+                const double work = items + stage + 1875.0 + 296.0 * T;  // fixed terms fitted on B200
+                const int64_t ctas = (int64_t)h->tiles_x * h->bands * h->R;
+                const int64_t per_sm = (ctas + nsm - 1) / nsm;
+                const double t = per_sm == 1 ? 0.6 * work : 0.5 * (double)per_sm * work;
+                if (t < best * 0.999) {
+                    best = t;
+                    bt = twi_t;
+                    bh = h->THI;
+                }
+            }
+        }
+        set_tiles(h, bt, bh);
+    }
+    const int64_t rows = h->g.rows, thi = h->THI;
     // slab mode: bands whose loaded rows [b*THI - hy, (b+1)*THI + hy) are local
     h->b_lo = (int)((h->hy + thi - 1) / thi);
     h->b_hi = (int)std::max<int64_t>(0, (rows - h->hy) / thi);
