@@ -24,7 +24,8 @@ void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 int pass_smem_bytes(int T, int THI, int TWI);
 int resident_smem_bytes(const Geom& g);
-cudaError_t launch_resident(const ResParams& P, int64_t replicas, cudaStream_t stream);
+int resident_threads(const Geom& g, int64_t replicas, int nsm, int forced);
+cudaError_t launch_resident(const ResParams& P, int64_t replicas, int nt, cudaStream_t stream);
 cudaError_t launch_pass(int T, const PassParams& P, const CUtensorMap& tmap, int grid_y, int replicas,
                         cudaStream_t stream);
 cudaError_t launch_observe(const ObsParams& P, cudaStream_t s);
@@ -71,6 +72,7 @@ struct kk_lattice {
     int THI = 0, TWI = 0, tiles_x = 0, bands = 0, b_lo = 0, b_hi = 0;
     int use_tma = 0, box_h = 0;
     int resident = 0;                 // kk_sweep runs the resident kernel (whole replica in shared memory)
+    int res_nt = 512;                 // its CTA size
     CUtensorMap tmap[2];              // TMA descriptors of buf[0], buf[1]
     // cluster analysis workspace (lazy)
     uint32_t* edges = nullptr;
@@ -471,11 +473,19 @@ int kk_create_ex(kk_handle* out, const kk_config* c) {
     {
         // resident kernel: one CTA per replica, all sweeps of a kk_sweep call in
         // one launch.  Auto (KK_RESIDENT=1, default) when the tile kernel would
-        // not spread a replica over more than two CTAs anyway; 2 = whenever the
-        // replica fits; 0 = never.
+        // not spread a replica over more than two CTAs anyway, or when there
+        // are enough replicas to fill every SM; 2 = whenever the replica fits;
+        // 0 = never.
         const int mode = env_int("KK_RESIDENT", 1);
         const int64_t tile_ctas = (int64_t)h->tiles_x * h->bands;
-        h->resident = resident_smem_bytes(h->g) > 0 && (mode == 2 || (mode == 1 && tile_ctas <= 2)) ? 1 : 0;
+        int nsm = 148;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device);
+        if (nsm <= 0) nsm = 148;
+        h->resident = resident_smem_bytes(h->g) > 0 &&
+                              (mode == 2 || (mode == 1 && (tile_ctas <= 2 || h->R >= nsm)))
+                          ? 1
+                          : 0;
+        h->res_nt = resident_threads(h->g, h->R, nsm, env_int("KK_RES_THREADS", 0));
     }
     if (pass_smem_bytes(T, h->THI, h->TWI) > 227 * 1024) {
         delete h;
@@ -578,7 +588,7 @@ int kk_sweep(kk_handle h, int64_t n, void* stream) {
         P.key1 = Q.key1;
         for (int k = 0; k < 20; ++k) P.rk[k] = Q.rk[k];
         for (int k = 0; k < 7; ++k) P.thr[k] = Q.thr[k];
-        KK_CUDA(launch_resident(P, h->R, S(stream)));
+        KK_CUDA(launch_resident(P, h->R, h->res_nt, S(stream)));
         h->cur ^= 1;
         h->sweep += n;
         return KK_OK;

@@ -25,6 +25,8 @@
 // the result does not depend on thread scheduling).
 #include <cuda.h>  // CUtensorMap (TMA descriptor type only; no driver calls here)
 
+#include <algorithm>
+
 #include "kk_internal.cuh"
 
 namespace kk {
@@ -582,11 +584,12 @@ __device__ __forceinline__ uint32_t res_word(int base, int w, int W, int tail) {
     return kk_smem[base + w];
 }
 
+template <int NT>
 __device__ __forceinline__ void res_refresh(const Tabs& S) {
     const int W = S.rW, tail = S.rTail, rows = S.rRows, WS = S.WS;
     const int nx = tail ? 3 : 2;  // rewritten words of a real row: 0, W+1 (and W)
     const int n_real = rows * nx, total = n_real + 4 * (W + 2);
-    for (int i = threadIdx.x; i < total; i += kThreads) {
+    for (int i = threadIdx.x; i < total; i += NT) {
         int dst_row, src_row, w;
         if (i < n_real) {
             const int a = i / nx, k = i - a * nx;
@@ -604,16 +607,16 @@ __device__ __forceinline__ void res_refresh(const Tabs& S) {
     }
 }
 
-template <int KX>
+template <int KX, int NT>
 __device__ __forceinline__ void res_iteration(const Tabs& S, int r_first, uint32_t sweep, uint32_t c3,
                                               const uint32_t* rk, Acc& acc) {
     const int W = S.rW;
     const int items = (S.rRows / 4) * W;
     int a = threadIdx.x / W;
     int w = threadIdx.x - a * W;
-    const int da = kThreads / W, dw = kThreads - da * W;
+    const int da = NT / W, dw = NT - da * W;
     int since_flush = 0;
-    for (int it = threadIdx.x; it < items; it += kThreads) {
+    for (int it = threadIdx.x; it < items; it += NT) {
         process_item<KX, true>(S, r_first + 4 * a, w + 1, sweep, c3, rk, acc);
         if (++since_flush == 32) {
             acc_flush(acc);
@@ -628,7 +631,8 @@ __device__ __forceinline__ void res_iteration(const Tabs& S, int r_first, uint32
     }
 }
 
-__global__ void __launch_bounds__(kThreads, kMinBlocks) resident_kernel(const ResParams P) {
+template <int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT) resident_kernel(const ResParams P) {
     const int rep = blockIdx.x;
     const Geom& g = P.g;
     const int W = g.W, tail = g.tail, rows = (int)g.rows;
@@ -646,9 +650,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) resident_kernel(const Re
     unsigned long long* red = reinterpret_cast<unsigned long long*>(kk_smem + S.th_off + 512);
     uint2* thr2 = reinterpret_cast<uint2*>(kk_smem + S.th_off);
     uint2* mtab = reinterpret_cast<uint2*>(kk_smem + S.mt_off);
-    for (int b = threadIdx.x; b < 256; b += kThreads)
+    for (int b = threadIdx.x; b < 256; b += NT)
         thr2[b] = make_uint2(P.thr[min(b & 15, 6)], P.thr[min(b >> 4, 6)]);
-    for (int w = threadIdx.x; w < Wt; w += kThreads) {
+    for (int w = threadIdx.x; w < Wt; w += NT) {
         // every real word starts an aligned octet (x = 32(w-1)); in a partial
         // last word the centres past Lx are masked out of wm
         mtab[w] = make_uint2(w >= 1 ? 32u * (uint32_t)(w - 1) : 0u, 1u);
@@ -656,23 +660,23 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) resident_kernel(const Re
         if (w >= 1 && w <= W) own = (w == W && tail) ? ((1u << tail) - 1u) : 0xFFFFFFFFu;
         kk_smem[S.wm_off + w] = own;
     }
-    for (int r = threadIdx.x; r < H; r += kThreads)
+    for (int r = threadIdx.x; r < H; r += NT)
         kk_smem[S.rl_off + r] = (r >= 2 && r < rows + 2) ? ((uint32_t)((r - 2) >> 2) | 0x80000000u) : 0u;
     // stage the replica
     const uint32_t* src = P.src + rep * g.rep_words;
-    for (int i = threadIdx.x; i < rows * W; i += kThreads) {
+    for (int i = threadIdx.x; i < rows * W; i += NT) {
         const int y = i / W, x = i - y * W;
         kk_smem[(y + 2) * WS + kCol0 + 1 + x] = src[i];
     }
     __syncthreads();
-    res_refresh(S);
+    res_refresh<NT>(S);
     __syncthreads();
 
     // per-warp 64-bit totals in shared memory (lane 0 of each warp adds its
     // warp's 32-bit sums once per sweep)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (lane == 0)
-        for (int k = 0; k < 4; ++k) red[k * (kThreads / 32) + warp] = 0ull;
+        for (int k = 0; k < 4; ++k) red[k * (NT / 32) + warp] = 0ull;
     Acc acc = {0u, 0u, 0u, 0u, 0u, 0ull};
     uint32_t sweep = P.sweep0;
     int j = P.j0;
@@ -688,14 +692,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) resident_kernel(const Re
             const int kx = (int)(k & 3u), ky = (int)(k >> 2);
             const uint32_t c3 = ((uint32_t)rep << 8) | (uint32_t)j;
             switch (kx) {
-                case 0: res_iteration<0>(S, 2 + ky, sweep, c3, P.rk, acc); break;
-                case 1: res_iteration<1>(S, 2 + ky, sweep, c3, P.rk, acc); break;
-                case 2: res_iteration<2>(S, 2 + ky, sweep, c3, P.rk, acc); break;
-                default: res_iteration<3>(S, 2 + ky, sweep, c3, P.rk, acc); break;
+                case 0: res_iteration<0, NT>(S, 2 + ky, sweep, c3, P.rk, acc); break;
+                case 1: res_iteration<1, NT>(S, 2 + ky, sweep, c3, P.rk, acc); break;
+                case 2: res_iteration<2, NT>(S, 2 + ky, sweep, c3, P.rk, acc); break;
+                default: res_iteration<3, NT>(S, 2 + ky, sweep, c3, P.rk, acc); break;
             }
             acc_flush(acc);
             __syncthreads();
-            res_refresh(S);
+            res_refresh<NT>(S);
             __syncthreads();
         }
         if (j == 16) {
@@ -712,10 +716,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) resident_kernel(const Re
             c3s += __shfl_xor_sync(0xFFFFFFFFu, c3s, o);
         }
         if (lane == 0) {
-            red[0 * (kThreads / 32) + warp] += c0;
-            red[1 * (kThreads / 32) + warp] += c1;
-            red[2 * (kThreads / 32) + warp] += c2;
-            red[3 * (kThreads / 32) + warp] += c3s;
+            red[0 * (NT / 32) + warp] += c0;
+            red[1 * (NT / 32) + warp] += c1;
+            red[2 * (NT / 32) + warp] += c2;
+            red[3 * (NT / 32) + warp] += c3s;
         }
         acc.attempted = acc.trivial = acc.accepted = 0u;
         acc.idx_sum = 0ull;
@@ -724,7 +728,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) resident_kernel(const Re
     // write back the real words
     uint32_t* dst = P.dst + rep * g.rep_words;
     const uint32_t last = tail ? ((1u << tail) - 1u) : 0xFFFFFFFFu;
-    for (int i = threadIdx.x; i < rows * W; i += kThreads) {
+    for (int i = threadIdx.x; i < rows * W; i += NT) {
         const int y = i / W, x = i - y * W;
         const uint32_t v = kk_smem[(y + 2) * WS + kCol0 + 1 + x];
         dst[i] = x == W - 1 ? (v & last) : v;
@@ -732,13 +736,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) resident_kernel(const Re
 
     // dN_AB total = 2 (sum of idx - 3 per accepted centre)
     if (lane == 0)
-        red[3 * (kThreads / 32) + warp] =
-            (unsigned long long)(2 * ((long long)red[3 * (kThreads / 32) + warp] -
-                                      3 * (long long)red[2 * (kThreads / 32) + warp]));
+        red[3 * (NT / 32) + warp] =
+            (unsigned long long)(2 * ((long long)red[3 * (NT / 32) + warp] -
+                                      3 * (long long)red[2 * (NT / 32) + warp]));
     __syncthreads();
     if (threadIdx.x < 4) {
         unsigned long long s = 0;
-        for (int k = 0; k < kThreads / 32; ++k) s += red[threadIdx.x * (kThreads / 32) + k];
+        for (int k = 0; k < NT / 32; ++k) s += red[threadIdx.x * (NT / 32) + k];
         if (s) atomicAdd(P.stats + rep * 4 + threadIdx.x, s);
     }
 }
@@ -758,16 +762,39 @@ int resident_smem_bytes(const Geom& g) {
     const int64_t H = g.rows + 4, Wt = g.W + 2, WS = Wt + kCol0;
     const int64_t tile_words = (H * WS + 1) & ~1;
     const int64_t th_off = (tile_words + 2 * Wt + Wt + H + 1) & ~1;
-    const int64_t bytes = 4 * (th_off + 512 + 2 * 4 * (kThreads / 32));
+    const int64_t bytes = 4 * (th_off + 512 + 2 * 4 * (512 / 32));
     return bytes <= 227 * 1024 ? (int)bytes : 0;
 }
 
-cudaError_t launch_resident(const ResParams& P, int64_t replicas, cudaStream_t stream) {
+// CTA size (measured on B200, tools/res_threads.py): 512 threads while all
+// replicas fit on the GPU at once at 2 CTAs/SM; beyond one wave 256 (4
+// CTAs/SM hide the per-iteration barriers better), unless an iteration has
+// too few work items (tiny replicas), then 128.  KK_RES_THREADS overrides.
+int resident_threads(const Geom& g, int64_t replicas, int nsm, int forced) {
+    if (forced == 128 || forced == 256 || forced == 512) return forced;
+    const int64_t items = (g.rows / 4) * (int64_t)g.W;  // work items per iteration
+    if (replicas <= 2 * (int64_t)nsm) return 512;
+    return items >= 512 ? 256 : 128;
+}
+
+cudaError_t launch_resident(const ResParams& P, int64_t replicas, int nt, cudaStream_t stream) {
     const int smem = resident_smem_bytes(P.g);
     if (!smem) return cudaErrorInvalidValue;
-    cudaError_t e = cudaFuncSetAttribute(resident_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    resident_kernel<<<(unsigned)replicas, kThreads, smem, stream>>>(P);
+    cudaError_t e = cudaSuccess;
+#define KK_RES(NTT)                                                                                    \
+    case NTT:                                                                                          \
+        e = cudaFuncSetAttribute(resident_kernel<NTT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+        if (e != cudaSuccess) return e;                                                                \
+        resident_kernel<NTT><<<(unsigned)replicas, NTT, smem, stream>>>(P);                            \
+        break;
+    switch (nt) {
+        KK_RES(128)
+        KK_RES(256)
+        KK_RES(512)
+        default:
+            return cudaErrorInvalidValue;
+    }
+#undef KK_RES
     count_launch();
     return cudaGetLastError();
 }

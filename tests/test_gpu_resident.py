@@ -88,3 +88,10 @@ def test_config3_replica_batch_sample():
         ost = O.run(ref, om, seed, 2, replica=r)
         assert np.array_equal(got[r], ref), r
         assert list(st[r]) == [ost["attempted"], ost["trivial"], ost["accepted"], ost["dnab_sum"]]
+
+
+@pytest.mark.parametrize("nt", [128, 256, 512])
+@pytest.mark.parametrize("Lx,Ly,R", [(100, 20, 3), (400, 40, 2), (64, 64, 5)])
+def test_resident_cta_sizes(Lx, Ly, R, nt):
+    """All resident CTA sizes (KK_RES_THREADS) give the oracle's result."""
+    _run_parity(Lx, Ly, 0.4, 0.8, 5 + nt, 4, R=R, env={"KK_RESIDENT": 2, "KK_RES_THREADS": nt})
