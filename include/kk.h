@@ -114,7 +114,8 @@ int kk_stats(kk_handle h, int64_t* out, int reset, void* stream);
  * `target` (1 = A, 0 = B) sites connected through the six neighbours on the
  * periodic lattice.  Writes rows (replica, size, count) sorted by replica then
  * size to out (host, 3*capacity int64); *n_out = rows written.  If capacity is
- * too small returns KK_ERR_CAPACITY with *n_out = rows needed.  Full-lattice
+ * too small returns KK_ERR_CAPACITY with *n_out = rows needed (a retry
+ * labels the lattice again, so callers should size generously).  Full-lattice
  * handles only. */
 int kk_cluster_histogram(kk_handle h, int target, int64_t* out, int64_t capacity,
                          int64_t* n_out, void* stream);

@@ -204,11 +204,14 @@ class Lattice:
         """Per replica: sorted list of (size, count)."""
         lib = load()
         n = _i64()
-        cap = 4096
+        # start from twice the last size seen: a too-small buffer makes the
+        # library relabel the lattice on the retry
+        cap = max(8192, 2 * getattr(self, "_hist_rows", 0))
         while True:
             buf = np.zeros((cap, 3), np.int64)
             rc = lib.kk_cluster_histogram(self._h, int(target), buf.ctypes.data, cap, ctypes.byref(n),
                                           stream_ptr(stream))
+            self._hist_rows = max(getattr(self, "_hist_rows", 0), int(n.value))
             if rc == -4 and n.value > cap:
                 cap = int(n.value)
                 continue
@@ -264,11 +267,12 @@ class Lattice:
         """Slab-local clusters: returns (complete rows [(size, count)], n_open)."""
         lib = load()
         nh, no = _i64(), _i64()
-        cap = 4096
+        cap = max(8192, 2 * getattr(self, "_slab_rows", 0))   # a retry relabels the slab
         while True:
             buf = np.zeros((cap, 2), np.int64)
             rc = lib.kk_cluster_slab(self._h, int(target), buf.ctypes.data, cap, ctypes.byref(nh), top_ids,
                                      bot_ids, open_sizes, int(open_cap), ctypes.byref(no), stream_ptr(stream))
+            self._slab_rows = max(getattr(self, "_slab_rows", 0), int(nh.value))
             if rc == -4 and nh.value > cap:
                 cap = int(nh.value)
                 continue
