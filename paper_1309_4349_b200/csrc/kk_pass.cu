@@ -176,7 +176,9 @@ struct Tabs {
 // copies in guard rows/words): only owned centres flip, and a flip that lands
 // on a copy is applied to the true site instead (copies are rebuilt after
 // every iteration).
-template <int KX, bool RES = false>
+// FAST = every word of the tile is an aligned octet (checked per CTA), so the
+// per-centre draw path is compiled out and the item is one basic block.
+template <int KX, bool RES = false, bool FAST = false>
 __device__ __forceinline__ void process_item(const Tabs& S, int r, int w, uint32_t sweep, uint32_t c3,
                                              const uint32_t* rk, Acc& acc) {
     const uint32_t rl = kk_smem[S.rl_off + r];
@@ -185,9 +187,12 @@ __device__ __forceinline__ void process_item(const Tabs& S, int r, int w, uint32
     // ---- random draws (R6): octet g of 8 centres; call 4g gives the four
     // pair-direction words (q = w*36 >> 32 -> d_even = q/6, d_odd = q%6),
     // calls 4g+1, 4g+2 the eight acceptance uniforms.
+    // FAST: the octet draws have no branch around them, so they and the SWAR
+    // neighbourhood work below form one basic block the scheduler can
+    // interleave (Philox is IMAD-heavy, the SWAR part LOP3/SHF-heavy).
     uint32_t u[8];
     uint32_t dv = 0;  // direction nibble vector: nibble q = direction of centre q
-    if (mq.y) {       // the word is one whole octet (common case)
+    if (FAST || mq.y) {  // the word is one whole octet (common case)
         const uint32_t g4 = (mq.x >> 5) * 4u;
         const uint32_t m[3] = {g4, g4 + 1u, g4 + 2u};
         uint32_t R3[3][4];
@@ -200,7 +205,7 @@ __device__ __forceinline__ void process_item(const Tabs& S, int r, int w, uint32
             u[p] = R3[1][p];
             u[4 + p] = R3[2][p];
         }
-    } else {          // word straddles an octet boundary (x wrap, Lx % 32 != 0, tiny Lx)
+    } else {  // word straddles an octet boundary (x wrap, Lx % 32 != 0, tiny Lx)
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
             uint32_t x = mq.x + 4u * q + KX;
@@ -352,7 +357,7 @@ __device__ __forceinline__ void process_item(const Tabs& S, int r, int w, uint32
     acc.idx_odd += (Sg >> 4) & 0x0F0F0F0Fu;
 }
 
-template <int KX>
+template <int KX, bool FAST>
 __device__ __forceinline__ void run_iteration(const Tabs& S, int Wt, int r_first, int nrows, uint32_t sweep,
                                               uint32_t c3, const uint32_t* rk, Acc& acc) {
     const int items = nrows * Wt;
@@ -362,7 +367,7 @@ __device__ __forceinline__ void run_iteration(const Tabs& S, int Wt, int r_first
     const int da = kThreads / Wt, dw = kThreads - da * Wt;
     int since_flush = 0;
     for (int it = threadIdx.x; it < items; it += kThreads) {
-        process_item<KX>(S, r_first + 4 * a, w, sweep, c3, rk, acc);
+        process_item<KX, false, FAST>(S, r_first + 4 * a, w, sweep, c3, rk, acc);
         if (++since_flush == 32) {
             acc_flush(acc);
             since_flush = 0;
@@ -376,7 +381,9 @@ __device__ __forceinline__ void run_iteration(const Tabs& S, int Wt, int r_first
     }
 }
 
-template <int T>
+// FAST: Lx % 32 == 0, so every tile word (halo words included) is an
+// aligned octet of centres and the per-centre draw path is compiled out.
+template <int T, bool FAST>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
     pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassParams P) {
     constexpr int HY = 3 * T;
@@ -498,10 +505,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
         const int r_first = r_lo + ((phase - r_lo) & 3);
         const int nrows = r_hi > r_first ? (r_hi - r_first + 3) / 4 : 0;
         switch (kx) {
-            case 0: run_iteration<0>(S, Wt, r_first, nrows, P.sweep, c3, P.rk, acc); break;
-            case 1: run_iteration<1>(S, Wt, r_first, nrows, P.sweep, c3, P.rk, acc); break;
-            case 2: run_iteration<2>(S, Wt, r_first, nrows, P.sweep, c3, P.rk, acc); break;
-            default: run_iteration<3>(S, Wt, r_first, nrows, P.sweep, c3, P.rk, acc); break;
+            case 0: run_iteration<0, FAST>(S, Wt, r_first, nrows, P.sweep, c3, P.rk, acc); break;
+            case 1: run_iteration<1, FAST>(S, Wt, r_first, nrows, P.sweep, c3, P.rk, acc); break;
+            case 2: run_iteration<2, FAST>(S, Wt, r_first, nrows, P.sweep, c3, P.rk, acc); break;
+            default: run_iteration<3, FAST>(S, Wt, r_first, nrows, P.sweep, c3, P.rk, acc); break;
         }
         acc_flush(acc);
         __syncthreads();
@@ -617,7 +624,7 @@ __device__ __forceinline__ void res_iteration(const Tabs& S, int r_first, uint32
     const int da = NT / W, dw = NT - da * W;
     int since_flush = 0;
     for (int it = threadIdx.x; it < items; it += NT) {
-        process_item<KX, true>(S, r_first + 4 * a, w + 1, sweep, c3, rk, acc);
+        process_item<KX, true, true>(S, r_first + 4 * a, w + 1, sweep, c3, rk, acc);
         if (++since_flush == 32) {
             acc_flush(acc);
             since_flush = 0;
@@ -807,9 +814,15 @@ cudaError_t launch_pass(int T, const PassParams& P, const CUtensorMap& tmap, int
     cudaError_t e = cudaSuccess;
 #define KK_LAUNCH(TT)                                                                                  \
     case TT:                                                                                           \
-        e = cudaFuncSetAttribute(pass_kernel<TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
-        if (e != cudaSuccess) return e;                                                                \
-        pass_kernel<TT><<<grid, kThreads, smem, stream>>>(tmap, P);                                          \
+        if (P.g.tail == 0) {                                                                           \
+            e = cudaFuncSetAttribute(pass_kernel<TT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+            if (e != cudaSuccess) return e;                                                            \
+            pass_kernel<TT, true><<<grid, kThreads, smem, stream>>>(tmap, P);                          \
+        } else {                                                                                       \
+            e = cudaFuncSetAttribute(pass_kernel<TT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+            if (e != cudaSuccess) return e;                                                            \
+            pass_kernel<TT, false><<<grid, kThreads, smem, stream>>>(tmap, P);                         \
+        }                                                                                              \
         break;
     switch (T) {
         KK_LAUNCH(1)
