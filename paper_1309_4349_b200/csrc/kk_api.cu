@@ -23,6 +23,8 @@ static std::atomic<long long> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 int pass_smem_bytes(int T, int THI, int TWI);
+void set_pass_layout(int T, PassParams& P);
+void set_resident_layout(ResParams& P);
 int resident_smem_bytes(const Geom& g);
 int resident_threads(const Geom& g, int64_t replicas, int nsm, int forced);
 cudaError_t launch_resident(const ResParams& P, int64_t replicas, int nt, cudaStream_t stream);
@@ -219,6 +221,7 @@ PassParams make_pass_params(kk_lattice* h, const uint32_t* ht, const uint32_t* h
         P.rk[10 + r] = P.key1 + (uint32_t)r * 0xBB67AE85u;
     }
     for (int k = 0; k < 7; ++k) P.thr[k] = h->thr[k];
+    set_pass_layout(h->T, P);
     P.use_tma = h->use_tma;
     P.box_h = h->box_h;
     P.vec_wb = (h->g.tail == 0 && h->g.W % 4 == 0 && h->TWI % 4 == 0) ? 1 : 0;
@@ -588,6 +591,7 @@ int kk_sweep(kk_handle h, int64_t n, void* stream) {
         P.key1 = Q.key1;
         for (int k = 0; k < 20; ++k) P.rk[k] = Q.rk[k];
         for (int k = 0; k < 7; ++k) P.thr[k] = Q.thr[k];
+        set_resident_layout(P);
         KK_CUDA(launch_resident(P, h->R, h->res_nt, S(stream)));
         h->cur ^= 1;
         h->sweep += n;

@@ -130,6 +130,7 @@ struct PassParams {
     int32_t use_tma;           // interior tiles staged by cp.async.bulk.tensor (tensor map = src)
     int32_t box_h;             // rows per TMA box
     int32_t vec_wb;            // write-back with 16-byte vectors (W % 4 == 0, TWI % 4 == 0, no tail)
+    int32_t mt_off, wm_off, rl_off, th_off, dt_off, red_off;  // shared-memory layout (smem_layout)
 };
 
 // Resident kernel (kk_pass.cu): one CTA holds one whole replica in shared
@@ -145,7 +146,30 @@ struct ResParams {
     uint32_t key0, key1;
     uint32_t rk[20];
     uint32_t thr[7];
+    int32_t mt_off, wm_off, rl_off, th_off, dt_off, red_off;  // shared-memory layout (smem_layout)
 };
+
+// Shared-memory layout of the pass and resident kernels (word offsets): the
+// tile (H rows x WS words) at 0, then the per-pass tables — centre-octet
+// table (uint2 [Wt]), ownership masks ([Wt]), centre-row table ([H]), pair
+// threshold table (uint2 [256]), pair direction table (uint16 [36*36]) — and
+// the reduction scratch ([4][16] uint64 + a TMA barrier).  Computed on the
+// host and passed in the kernel parameters, so every table base is a
+// constant-bank operand in the inner loop.
+struct SmemLayout {
+    int mt_off, wm_off, rl_off, th_off, dt_off, red_off, words;
+};
+inline SmemLayout smem_layout(int H, int Wt, int WS) {
+    SmemLayout L;
+    L.mt_off = (H * WS + 1) & ~1;
+    L.wm_off = L.mt_off + 2 * Wt;
+    L.rl_off = L.wm_off + Wt;
+    L.th_off = (L.rl_off + H + 1) & ~1;
+    L.dt_off = L.th_off + 512;
+    L.red_off = (L.dt_off + 648 + 1) & ~1;
+    L.words = L.red_off + 2 * 4 * 16 + 2;
+    return L;
+}
 
 struct ObsParams {
     const uint32_t* lat;

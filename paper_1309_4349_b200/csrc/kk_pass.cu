@@ -166,10 +166,22 @@ struct Tabs {
     int wm_off;                // uint32 [Wt]: owned bits of the word (0 for halo words)
     int rl_off;                // uint32 [H]: centre-row index l | owned-row flag << 31
     int th_off;                // uint2 [256]: thresholds of the two nibbles of a byte of idx
+    int dt_off;                // uint16 [36*36]: direction nibbles of two centre pairs from (q_a, q_b)
     uint32_t Lx;
     int WS;
     int rW, rTail, rRows;      // resident kernel: lattice words, Lx % 32, rows (tile kernel: unused)
 };
+
+// Pair direction table (R6): entry qa*36 + qb = the direction nibbles of two
+// centre pairs, byte 0 = (qa/6) | (qa%6) << 4, byte 1 likewise for qb.
+template <int NT>
+__device__ __forceinline__ void fill_dir_table(const Tabs& S) {
+    uint16_t* dt = reinterpret_cast<uint16_t*>(kk_smem + S.dt_off);
+    for (int i = threadIdx.x; i < 36 * 36; i += NT) {
+        const uint32_t qa = (uint32_t)i / 36u, qb = (uint32_t)i % 36u;
+        dt[i] = (uint16_t)((qa / 6u) | ((qa % 6u) << 4) | ((qb / 6u) << 8) | ((qb % 6u) << 12));
+    }
+}
 
 // One work item: the 8 centres of tile word w (column w+1) in row r.
 // RES = the resident kernel's layout (whole replica in shared memory, wrapped
@@ -199,12 +211,15 @@ __device__ __forceinline__ void process_item(const Tabs& S, int r, int w, uint32
         philox10_xn<3>(m, l, sweep, c3, rk, R3);
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
-            const uint32_t q = __umulhi(R3[0][p], 36u);
-            const uint32_t de = (q * 43u) >> 8;  // q / 6 for q < 36
-            dv |= (de << (8 * p)) | ((q - 6u * de) << (8 * p + 4));
             u[p] = R3[1][p];
             u[4 + p] = R3[2][p];
         }
+        // pair p's direction word w gives q = w*36 >> 32 in [0, 36): d = q/6 for
+        // the even centre, q%6 for the odd one; two pairs per table lookup
+        const uint16_t* dt = reinterpret_cast<const uint16_t*>(kk_smem + S.dt_off);
+        const uint32_t q0 = __umulhi(R3[0][0], 36u), q1 = __umulhi(R3[0][1], 36u);
+        const uint32_t q2 = __umulhi(R3[0][2], 36u), q3 = __umulhi(R3[0][3], 36u);
+        dv = (uint32_t)dt[q0 * 36u + q1] | ((uint32_t)dt[q2 * 36u + q3] << 16);
     } else {  // word straddles an octet boundary (x wrap, Lx % 32 != 0, tiny Lx)
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -402,16 +417,18 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     Tabs S;
     S.WS = WS;
     S.Lx = (uint32_t)g.Lx;
-    S.mt_off = (H * WS + 1) & ~1;     // uint2 table, 8-byte aligned
-    S.wm_off = S.mt_off + 2 * Wt;
-    S.rl_off = S.wm_off + Wt;
-    S.th_off = (S.rl_off + H + 1) & ~1;
-    unsigned long long* red = reinterpret_cast<unsigned long long*>(kk_smem + S.th_off + 512);  // [4][warps]
-    uint64_t* tma_bar = reinterpret_cast<uint64_t*>(red + 4 * (kThreads / 32));
+    S.mt_off = P.mt_off;
+    S.wm_off = P.wm_off;
+    S.rl_off = P.rl_off;
+    S.th_off = P.th_off;
+    S.dt_off = P.dt_off;
+    unsigned long long* red = reinterpret_cast<unsigned long long*>(kk_smem + P.red_off);  // [4][warps]
+    uint64_t* tma_bar = reinterpret_cast<uint64_t*>(red + 4 * 16);
     uint2* thr2 = reinterpret_cast<uint2*>(kk_smem + S.th_off);
     uint2* mtab = reinterpret_cast<uint2*>(kk_smem + S.mt_off);
     for (int b = threadIdx.x; b < 256; b += kThreads)
         thr2[b] = make_uint2(P.thr[min(b & 15, 6)], P.thr[min(b >> 4, 6)]);
+    fill_dir_table<kThreads>(S);
 
     // ---- per-pass tables
     for (int w = threadIdx.x; w < Wt; w += kThreads) {
@@ -650,15 +667,17 @@ __global__ void __launch_bounds__(NT, 1024 / NT) resident_kernel(const ResParams
     S.rW = W;
     S.rTail = tail;
     S.rRows = rows;
-    S.mt_off = (H * WS + 1) & ~1;
-    S.wm_off = S.mt_off + 2 * Wt;
-    S.rl_off = S.wm_off + Wt;
-    S.th_off = (S.rl_off + H + 1) & ~1;
-    unsigned long long* red = reinterpret_cast<unsigned long long*>(kk_smem + S.th_off + 512);
+    S.mt_off = P.mt_off;
+    S.wm_off = P.wm_off;
+    S.rl_off = P.rl_off;
+    S.th_off = P.th_off;
+    S.dt_off = P.dt_off;
+    unsigned long long* red = reinterpret_cast<unsigned long long*>(kk_smem + P.red_off);
     uint2* thr2 = reinterpret_cast<uint2*>(kk_smem + S.th_off);
     uint2* mtab = reinterpret_cast<uint2*>(kk_smem + S.mt_off);
     for (int b = threadIdx.x; b < 256; b += NT)
         thr2[b] = make_uint2(P.thr[min(b & 15, 6)], P.thr[min(b >> 4, 6)]);
+    fill_dir_table<NT>(S);
     for (int w = threadIdx.x; w < Wt; w += NT) {
         // every real word starts an aligned octet (x = 32(w-1)); in a partial
         // last word the centres past Lx are masked out of wm
@@ -758,18 +777,37 @@ __global__ void __launch_bounds__(NT, 1024 / NT) resident_kernel(const ResParams
 
 int pass_smem_bytes(int T, int THI, int TWI) {
     const int H = THI + 6 * T, Wt = TWI + 2, WS = Wt + 6;
-    const int tile_words = (H * WS + 1) & ~1;
-    const int th_off = (tile_words + 2 * Wt + Wt + H + 1) & ~1;
-    return 4 * (th_off + 512 + 2 * 4 * (kThreads / 32) + 2);
+    return 4 * smem_layout(H, Wt, WS).words;
+}
+
+void set_pass_layout(int T, PassParams& P) {
+    const int H = P.THI + 6 * T, Wt = P.TWI + 2, WS = Wt + 6;
+    const SmemLayout L = smem_layout(H, Wt, WS);
+    P.mt_off = L.mt_off;
+    P.wm_off = L.wm_off;
+    P.rl_off = L.rl_off;
+    P.th_off = L.th_off;
+    P.dt_off = L.dt_off;
+    P.red_off = L.red_off;
+}
+
+void set_resident_layout(ResParams& P) {
+    const int H = (int)P.g.rows + 4, Wt = P.g.W + 2, WS = Wt + kCol0;
+    const SmemLayout L = smem_layout(H, Wt, WS);
+    P.mt_off = L.mt_off;
+    P.wm_off = L.wm_off;
+    P.rl_off = L.rl_off;
+    P.th_off = L.th_off;
+    P.dt_off = L.dt_off;
+    P.red_off = L.red_off;
 }
 
 // 0 if the replica does not fit (or the layout needs Lx >= 64, W >= 3 with a tail)
 int resident_smem_bytes(const Geom& g) {
     if (g.Lx < 64 || (g.tail && g.W < 3) || !g.periodic) return 0;
     const int64_t H = g.rows + 4, Wt = g.W + 2, WS = Wt + kCol0;
-    const int64_t tile_words = (H * WS + 1) & ~1;
-    const int64_t th_off = (tile_words + 2 * Wt + Wt + H + 1) & ~1;
-    const int64_t bytes = 4 * (th_off + 512 + 2 * 4 * (512 / 32));
+    if (H * WS > 227 * 256) return 0;
+    const int64_t bytes = 4 * (int64_t)smem_layout((int)H, (int)Wt, (int)WS).words;
     return bytes <= 227 * 1024 ? (int)bytes : 0;
 }
 
