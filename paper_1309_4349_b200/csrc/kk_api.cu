@@ -49,6 +49,10 @@ cudaError_t launch_ccl(const uint32_t* lat, const Geom& g, int64_t replicas, int
                        unsigned long long* root_size, unsigned int* counter, unsigned int* hist,
                        unsigned long long* big, unsigned long long* nbig, int64_t big_cap, cudaStream_t s,
                        const SlabCclArgs* slab);
+cudaError_t launch_hist_compact(const unsigned int* hist, int64_t R, unsigned int* rep_rows,
+                                unsigned long long* row_off, cudaStream_t s);
+cudaError_t launch_hist_emit(const unsigned int* hist, int64_t R, const unsigned long long* row_off,
+                             unsigned long long* rows, cudaStream_t s);
 cudaError_t launch_join(int64_t Lx, int64_t nslabs, const uint32_t* top, const uint32_t* bot, const uint32_t* off,
                         const unsigned long long* sizes, int64_t n, uint32_t* par, unsigned long long* rsize,
                         unsigned long long* out, unsigned int* nout, cudaStream_t s);
@@ -90,6 +94,10 @@ struct kk_lattice {
     unsigned long long* big = nullptr;
     unsigned long long* nbig = nullptr;
     int64_t big_cap = 0;
+    unsigned int* rep_rows = nullptr;       // [R] nonzero dense bins per replica
+    unsigned long long* row_off = nullptr;  // [R+1] their exclusive scan
+    unsigned long long* rows_buf = nullptr; // compact dense rows (size << 32 | count)
+    int64_t rows_cap = 0;
 };
 
 namespace {
@@ -295,6 +303,9 @@ void free_all(kk_lattice* h) {
     cudaFree(h->hist);
     cudaFree(h->big);
     cudaFree(h->nbig);
+    cudaFree(h->rep_rows);
+    cudaFree(h->row_off);
+    cudaFree(h->rows_buf);
 }
 
 // ---- exact-composition random start (R7): radix select in three steps.
@@ -680,35 +691,56 @@ int ensure_ccl_workspace(kk_lattice* h) {
         cudaMalloc(&h->compact, 4 * nn) || cudaMalloc(&h->open_count, sizeof(unsigned int)) ||
         cudaMalloc(&h->hist, sizeof(unsigned int) * kDense * h->R) ||
         cudaMalloc(&h->big, sizeof(unsigned long long) * 2 * h->big_cap) ||
-        cudaMalloc(&h->nbig, sizeof(unsigned long long))) {
+        cudaMalloc(&h->nbig, sizeof(unsigned long long)) || cudaMalloc(&h->rep_rows, sizeof(unsigned int) * h->R) ||
+        cudaMalloc(&h->row_off, sizeof(unsigned long long) * (h->R + 1))) {
         cudaGetLastError();
         return fail(KK_ERR_NOMEM, "cluster workspace: device allocation failed");
     }
     return KK_OK;
 }
 
-// Dense histogram + big list -> rows (replica, size, count) sorted.
+// Dense histogram + big list -> rows (replica, size, count) sorted.  The
+// dense part is compacted on the device (only nonzero bins are copied back).
 int collect_hist_rows(kk_lattice* h, cudaStream_t s, std::vector<int64_t>& rows) {
-    std::vector<unsigned int> hist((size_t)kDense * h->R);
-    unsigned long long nb = 0;
-    KK_CUDA(cudaMemcpyAsync(hist.data(), h->hist, sizeof(unsigned int) * kDense * h->R, cudaMemcpyDeviceToHost, s));
+    const int64_t R = h->R;
+    KK_CUDA(launch_hist_compact(h->hist, R, h->rep_rows, h->row_off, s));
+    unsigned long long total = 0, nb = 0;
+    KK_CUDA(cudaMemcpyAsync(&total, h->row_off + R, sizeof(total), cudaMemcpyDeviceToHost, s));
     KK_CUDA(cudaMemcpyAsync(&nb, h->nbig, sizeof(nb), cudaMemcpyDeviceToHost, s));
     KK_CUDA(cudaStreamSynchronize(s));
     if ((int64_t)nb > h->big_cap) return fail(KK_ERR_STATE, "cluster list overflow");
-    std::vector<unsigned long long> big(2 * nb);
-    if (nb) {
-        KK_CUDA(cudaMemcpyAsync(big.data(), h->big, sizeof(unsigned long long) * 2 * nb, cudaMemcpyDeviceToHost, s));
-        KK_CUDA(cudaStreamSynchronize(s));
+    std::vector<unsigned long long> packed(total), off(R + 1);
+    if (total) {
+        if ((int64_t)total > h->rows_cap) {
+            cudaFree(h->rows_buf);
+            h->rows_buf = nullptr;
+            h->rows_cap = 0;
+            KK_CUDA(cudaMalloc(&h->rows_buf, sizeof(unsigned long long) * total));
+            h->rows_cap = (int64_t)total;
+        }
+        KK_CUDA(launch_hist_emit(h->hist, R, h->row_off, h->rows_buf, s));
+        KK_CUDA(cudaMemcpyAsync(packed.data(), h->rows_buf, sizeof(unsigned long long) * total,
+                                cudaMemcpyDeviceToHost, s));
+        KK_CUDA(cudaMemcpyAsync(off.data(), h->row_off, sizeof(unsigned long long) * (R + 1),
+                                cudaMemcpyDeviceToHost, s));
     }
+    std::vector<unsigned long long> big(2 * nb);
+    if (nb)
+        KK_CUDA(cudaMemcpyAsync(big.data(), h->big, sizeof(unsigned long long) * 2 * nb, cudaMemcpyDeviceToHost, s));
+    KK_CUDA(cudaStreamSynchronize(s));
     std::vector<std::pair<int64_t, int64_t>> bigl(nb);
     for (unsigned long long k = 0; k < nb; ++k) bigl[k] = {(int64_t)big[2 * k], (int64_t)big[2 * k + 1]};
     std::sort(bigl.begin(), bigl.end());
     rows.clear();
+    rows.reserve(3 * (total + nb));
     size_t bi = 0;
-    for (int64_t r = 0; r < h->R; ++r) {
-        for (int sz = 1; sz < kDense; ++sz) {
-            const unsigned int c = hist[(size_t)r * kDense + sz];
-            if (c) { rows.push_back(r); rows.push_back(sz); rows.push_back(c); }
+    for (int64_t r = 0; r < R; ++r) {
+        if (total) {
+            for (unsigned long long k = off[r]; k < off[r + 1]; ++k) {
+                rows.push_back(r);
+                rows.push_back((int64_t)(packed[k] >> 32));
+                rows.push_back((int64_t)(packed[k] & 0xFFFFFFFFull));
+            }
         }
         while (bi < bigl.size() && bigl[bi].first == r) {
             const int64_t sz = bigl[bi].second;

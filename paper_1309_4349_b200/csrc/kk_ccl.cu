@@ -170,29 +170,61 @@ __global__ void __launch_bounds__(kThreads) ccl_tile_kernel(const CclParams P) {
         for (uint32_t m = st; m; m &= m - 1) {
             const int b = __ffs(m) - 1;
             lab[base + b] = base + b;
-            cnt[base + b] = 0;
         }
     }
     __syncthreads();
-    // unions between runs of rows r and r+1
-    for (int i = threadIdx.x; i < kTR * kTW; i += kThreads) {
+    // unions between runs of rows r and r+1.  The union points of a warp's 32
+    // words are compacted into a per-warp list (in the size table's space,
+    // unused until the next phase) so that every lane takes one union at a
+    // time instead of looping over its own word's points.
+    {
+        static_assert(kThreads == kTR * kTW, "one thread per tile word");
+        constexpr int kBuf = 256;                       // entries per warp and round
+        const int i = threadIdx.x, lane = i & 31;
+        uint32_t* ubuf = cnt32 + (i >> 5) * kBuf;
         const int r = i / kTW, w = i - r * kTW;
-        if (r + 1 >= h_tile) continue;
-        const uint32_t t0 = tb[i], t1 = tb[i + kTW], S0 = S[i], S1 = S[i + kTW];
-        const uint32_t t1n = (w + 1 < kTW) ? tb[i + kTW + 1] : 0u;
-        const uint32_t S1n = (w + 1 < kTW) ? S[i + kTW + 1] : 0u;
-        const uint32_t t1s = (t1 >> 1) | (t1n << 31);   // bit x <- site x+1 of row r+1
-        const uint32_t S1s = (S1 >> 1) | (S1n << 31);
-        const uint32_t V1 = t0 & t1 & (S0 | S1);        // (0,+1) union points
-        const uint32_t V2 = t0 & t1s & (S0 | S1s);      // (+1,+1) union points
-        for (uint32_t m = V1; m; m &= m - 1) {
-            const int x = 32 * w + __ffs(m) - 1;
-            union32(lab, run_start(S, r, x), run_start(S, r + 1, x));
+        uint32_t V1 = 0, V2 = 0;
+        if (r + 1 < h_tile) {
+            const uint32_t t0 = tb[i], t1 = tb[i + kTW], S0 = S[i], S1 = S[i + kTW];
+            const uint32_t t1n = (w + 1 < kTW) ? tb[i + kTW + 1] : 0u;
+            const uint32_t S1n = (w + 1 < kTW) ? S[i + kTW + 1] : 0u;
+            const uint32_t t1s = (t1 >> 1) | (t1n << 31);   // bit x <- site x+1 of row r+1
+            const uint32_t S1s = (S1 >> 1) | (S1n << 31);
+            V1 = t0 & t1 & (S0 | S1);                        // (0,+1) union points
+            V2 = t0 & t1s & (S0 | S1s);                      // (+1,+1) union points
         }
-        for (uint32_t m = V2; m; m &= m - 1) {
-            const int x = 32 * w + __ffs(m) - 1;
-            union32(lab, run_start(S, r, x), run_start(S, r + 1, x + 1));
+        const uint32_t n = __popc(V1) + __popc(V2);
+        uint32_t incl = n;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += t;
         }
+        const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        for (uint32_t base = 0; base < total; base += kBuf) {
+            // entry = r << 9 | x << 1 | bond type, x = site column in the tile
+            uint32_t k = incl - n;
+            if (k < base + kBuf && k + n > base) {
+                for (uint32_t m = V1; m; m &= m - 1, ++k)
+                    if (k >= base && k < base + kBuf) ubuf[k - base] = (uint32_t)(r << 9) | ((32u * w + __ffs(m) - 1) << 1);
+                for (uint32_t m = V2; m; m &= m - 1, ++k)
+                    if (k >= base && k < base + kBuf)
+                        ubuf[k - base] = (uint32_t)(r << 9) | ((32u * w + __ffs(m) - 1) << 1) | 1u;
+            }
+            __syncwarp();
+            const uint32_t cnt_r = min(total - base, (uint32_t)kBuf);
+            for (uint32_t j = lane; j < cnt_r; j += 32) {
+                const uint32_t e = ubuf[j];
+                const int er = (int)(e >> 9), ex = (int)((e >> 1) & 255u);
+                union32(lab, run_start(S, er, ex), run_start(S, er + 1, ex + (int)(e & 1u)));
+            }
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kTR * kTW; i += kThreads) {
+        const int base = (i / kTW) * kTX + 32 * (i % kTW);
+        for (uint32_t m = S[i]; m; m &= m - 1) cnt[base + __ffs(m) - 1] = 0;
     }
     __syncthreads();
     // sizes per root (one atomic per run segment) and edge-touch flags
@@ -490,6 +522,91 @@ cudaError_t launch_join(int64_t Lx, int64_t nslabs, const uint32_t* top, const u
     join_sum_kernel<<<gn, 256, 0, s>>>(par, sizes, rsize, n);
     join_roots_kernel<<<gn, 256, 0, s>>>(par, rsize, n, out, nout);
     for (int k = 0; k < 4; ++k) count_launch();
+    return cudaGetLastError();
+}
+
+// ---- dense histogram -> compact rows on the device ------------------------------
+// Per replica r: the nonzero bins (size 1..kDense-1) in size order are written
+// as (size << 32 | count) at row_off[r] ..; row_off = exclusive scan of the
+// per-replica counts.  Three small kernels; the host reads back only the rows.
+__global__ void hist_count_kernel(const unsigned int* hist, unsigned int* rep_rows) {
+    const int64_t r = blockIdx.x;
+    unsigned int c = 0;
+    for (int s = threadIdx.x; s < kDense; s += blockDim.x) c += (s > 0 && hist[r * kDense + s]) ? 1u : 0u;
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+    __shared__ unsigned int part[32];
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned int t = 0;
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += part[k];
+        rep_rows[r] = t;
+    }
+}
+
+__global__ void hist_scan_kernel(const unsigned int* rep_rows, unsigned long long* row_off, int64_t R) {
+    // one block of 1024 threads: chunked exclusive scan, row_off[R] = total
+    __shared__ unsigned long long carry;
+    __shared__ unsigned long long wsum[32];
+    if (threadIdx.x == 0) carry = 0ull;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int64_t b = 0; b < R; b += blockDim.x) {
+        const int64_t i = b + threadIdx.x;
+        unsigned long long v = i < R ? rep_rows[i] : 0ull, incl = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) wsum[warp] = incl;
+        __syncthreads();
+        if (warp == 0) {
+            unsigned long long x = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0ull, xi = x;
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long t = __shfl_up_sync(0xFFFFFFFFu, xi, o);
+                if (lane >= o) xi += t;
+            }
+            wsum[lane] = xi - x;  // exclusive warp offsets
+        }
+        __syncthreads();
+        if (i < R) row_off[i] = carry + wsum[warp] + incl - v;
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry += wsum[warp] + incl;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) row_off[R] = carry;
+}
+
+__global__ void hist_emit_kernel(const unsigned int* hist, const unsigned long long* row_off,
+                                 unsigned long long* rows, int64_t R) {
+    // one warp per replica: bins in order, ballot + popc for the slots
+    const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (r >= R) return;
+    unsigned long long o = row_off[r];
+    for (int s0 = 0; s0 < kDense; s0 += 32) {
+        const int s = s0 + lane;
+        const unsigned int c = s > 0 ? hist[r * kDense + s] : 0u;
+        const unsigned int m = __ballot_sync(0xFFFFFFFFu, c != 0u);
+        if (c) rows[o + __popc(m & ((1u << lane) - 1u))] = ((unsigned long long)s << 32) | c;
+        o += __popc(m);
+    }
+}
+
+cudaError_t launch_hist_compact(const unsigned int* hist, int64_t R, unsigned int* rep_rows,
+                                unsigned long long* row_off, cudaStream_t s) {
+    hist_count_kernel<<<(unsigned)R, 256, 0, s>>>(hist, rep_rows);
+    hist_scan_kernel<<<1, 1024, 0, s>>>(rep_rows, row_off, R);
+    count_launch();
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_hist_emit(const unsigned int* hist, int64_t R, const unsigned long long* row_off,
+                             unsigned long long* rows, cudaStream_t s) {
+    const unsigned gx = (unsigned)((R + 7) / 8);
+    hist_emit_kernel<<<gx, 256, 0, s>>>(hist, row_off, rows, R);
+    count_launch();
     return cudaGetLastError();
 }
 

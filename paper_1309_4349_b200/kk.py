@@ -218,10 +218,11 @@ class Lattice:
             _check(rc, "kk_cluster_histogram")
             break
         rows = buf[: n.value]
-        out = [[] for _ in range(self.replicas)]
-        for r, s, c in rows.tolist():
-            out[r].append((s, c))
-        return out
+        # rows are sorted by replica: split at the replica boundaries
+        cuts = np.searchsorted(rows[:, 0], np.arange(self.replicas + 1))
+        sizes, counts = rows[:, 1].tolist(), rows[:, 2].tolist()
+        return [list(zip(sizes[cuts[r]:cuts[r + 1]], counts[cuts[r]:cuts[r + 1]]))
+                for r in range(self.replicas)]
 
     def cluster_histogram_raw(self, target: int = 1, capacity: int = 1 << 16, stream=None):
         """Rows (replica, size, count) as an int64 array (no per-replica lists)."""
