@@ -25,6 +25,10 @@ void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 int pass_smem_bytes(int T, int THI, int TWI);
 void set_pass_layout(int T, PassParams& P);
 void set_resident_layout(ResParams& P);
+int band_smem_bytes(const Geom& g, int nbands);
+void set_band_layout(BandParams& P);
+int64_t band_xch_words(const Geom& g, int nbands);
+cudaError_t launch_band(const BandParams& P, cudaStream_t stream);
 int resident_smem_bytes(const Geom& g);
 int resident_threads(const Geom& g, int64_t replicas, int nsm, int forced);
 cudaError_t launch_resident(const ResParams& P, int64_t replicas, int nt, cudaStream_t stream);
@@ -79,6 +83,10 @@ struct kk_lattice {
     int use_tma = 0, box_h = 0;
     int resident = 0;                 // kk_sweep runs the resident kernel (whole replica in shared memory)
     int res_nt = 512;                 // its CTA size
+    int nbands = 0;                   // > 0: kk_sweep runs the band kernel (lattice resident across all SMs)
+    uint32_t* xch = nullptr;          // band kernel exchange rows
+    unsigned int* band_flags = nullptr;
+    unsigned int* band_error = nullptr;
     CUtensorMap tmap[2];              // TMA descriptors of buf[0], buf[1]
     // cluster analysis workspace (lazy)
     uint32_t* edges = nullptr;
@@ -306,6 +314,9 @@ void free_all(kk_lattice* h) {
     cudaFree(h->rep_rows);
     cudaFree(h->row_off);
     cudaFree(h->rows_buf);
+    cudaFree(h->xch);
+    cudaFree(h->band_flags);
+    cudaFree(h->band_error);
 }
 
 // ---- exact-composition random start (R7): radix select in three steps.
@@ -500,6 +511,13 @@ int kk_create_ex(kk_handle* out, const kk_config* c) {
                           ? 1
                           : 0;
         h->res_nt = resident_threads(h->g, h->R, nsm, env_int("KK_RES_THREADS", 0));
+        // band kernel: one replica too big for one SM, spread over all SMs'
+        // shared memory.  Opt-in (KK_BAND=2): measured on B200 it loses to the
+        // tile kernel below ~8192^2 and wins only ~3% at 12288^2 (the L2
+        // handshake per iteration costs ~3 us, tools/band_vs_tile.py).
+        const int bmode = env_int("KK_BAND", 0);
+        const int nb = (int)std::min<int64_t>(nsm, h->g.rows / 4);
+        if (!h->resident && h->R == 1 && bmode == 2 && band_smem_bytes(h->g, nb) > 0) h->nbands = nb;
     }
     if (pass_smem_bytes(T, h->THI, h->TWI) > 227 * 1024) {
         delete h;
@@ -510,6 +528,12 @@ int kk_create_ex(kk_handle* out, const kk_config* c) {
     cudaError_t e2 = cudaMalloc(&h->buf[1], words * 4);
     cudaError_t e3 = cudaMalloc(&h->stats, sizeof(unsigned long long) * 4 * h->R);
     cudaError_t e4 = cudaMalloc(&h->obs, sizeof(unsigned long long) * 2 * h->R);
+    if (h->nbands && !e4) {
+        e4 = cudaMalloc(&h->xch, 4 * band_xch_words(h->g, h->nbands));
+        if (!e4) e4 = cudaMalloc(&h->band_flags, sizeof(unsigned int) * h->nbands);
+        if (!e4) e4 = cudaMalloc(&h->band_error, sizeof(unsigned int));
+        if (!e4) e4 = cudaMemset(h->band_error, 0, sizeof(unsigned int));
+    }
     if (e1 || e2 || e3 || e4) {
         free_all(h);
         delete h;
@@ -588,6 +612,30 @@ int kk_sweep(kk_handle h, int64_t n, void* stream) {
     KK_CHECK_HANDLE(h);
     if (!h->g.periodic) return fail(KK_ERR_STATE, "kk_sweep: slab handle (use kk_pass)");
     if (n < 0) return fail(KK_ERR_ARG, "n must be >= 0");
+    if (h->nbands && n > 0) {
+        BandParams B{};
+        B.src = h->buf[h->cur];
+        B.dst = h->buf[h->cur ^ 1];
+        B.stats = h->stats;
+        B.g = h->g;
+        B.sweep0 = (uint32_t)h->sweep;
+        B.j0 = h->j;
+        B.n_iters = 16 * n;
+        const PassParams Q = make_pass_params(h, nullptr, nullptr);
+        B.key0 = Q.key0;
+        B.key1 = Q.key1;
+        for (int k = 0; k < 20; ++k) B.rk[k] = Q.rk[k];
+        for (int k = 0; k < 7; ++k) B.thr[k] = Q.thr[k];
+        B.nbands = h->nbands;
+        B.xch = h->xch;
+        B.flags = h->band_flags;
+        B.error = h->band_error;
+        set_band_layout(B);
+        KK_CUDA(launch_band(B, S(stream)));
+        h->cur ^= 1;
+        h->sweep += n;
+        return KK_OK;
+    }
     if (h->resident && n > 0) {
         ResParams P{};
         P.src = h->buf[h->cur];
@@ -672,7 +720,10 @@ int kk_stats(kk_handle h, int64_t* out, int reset, void* stream) {
     cudaStream_t s = S(stream);
     KK_CUDA(cudaMemcpyAsync(out, h->stats, sizeof(int64_t) * 4 * h->R, cudaMemcpyDeviceToHost, s));
     if (reset) KK_CUDA(cudaMemsetAsync(h->stats, 0, sizeof(unsigned long long) * 4 * h->R, s));
+    unsigned int band_err = 0;
+    if (h->band_error) KK_CUDA(cudaMemcpyAsync(&band_err, h->band_error, sizeof(band_err), cudaMemcpyDeviceToHost, s));
     KK_CUDA(cudaStreamSynchronize(s));
+    if (band_err) return fail(KK_ERR_CUDA, "band kernel: a neighbour band never published (exchange timed out)");
     return KK_OK;
 }
 

@@ -149,6 +149,29 @@ struct ResParams {
     int32_t mt_off, wm_off, rl_off, th_off, dt_off, red_off;  // shared-memory layout (smem_layout)
 };
 
+// Band kernel (kk_pass.cu): one CTA per row band of a full periodic lattice,
+// the whole lattice resident in shared memory across the GPU for all
+// iterations of a kk_sweep call; neighbouring bands exchange 3 boundary rows
+// per iteration through L2 (flags with release/acquire).
+struct BandParams {
+    const uint32_t* src;       // current lattice
+    uint32_t* dst;             // next lattice
+    unsigned long long* stats; // [1][4]
+    Geom g;
+    uint32_t sweep0;
+    int32_t j0;
+    int64_t n_iters;
+    uint32_t key0, key1;
+    uint32_t rk[20];
+    uint32_t thr[7];
+    int32_t mt_off, wm_off, rl_off, th_off, dt_off, red_off;  // shared-memory layout (smem_layout)
+    int32_t nbands;
+    int32_t max_rows;          // rows of the largest band
+    uint32_t* xch;             // [nbands][2 slots][2 sides][3 rows][W]
+    unsigned int* flags;       // [nbands]: last iteration published (1-based, zeroed per launch)
+    unsigned int* error;       // set if a neighbour never published (timeout)
+};
+
 // Shared-memory layout of the pass and resident kernels (word offsets): the
 // tile (H rows x WS words) at 0, then the per-pass tables — centre-octet
 // table (uint2 [Wt]), ownership masks ([Wt]), centre-row table ([H]), pair
@@ -167,7 +190,7 @@ inline SmemLayout smem_layout(int H, int Wt, int WS) {
     L.th_off = (L.rl_off + H + 1) & ~1;
     L.dt_off = L.th_off + 512;
     L.red_off = (L.dt_off + 648 + 1) & ~1;
-    L.words = L.red_off + 2 * 4 * 16 + 2;
+    L.words = L.red_off + 2 * 4 * 32 + 2;  // [4][up to 32 warps] uint64 + TMA barrier
     return L;
 }
 

@@ -184,13 +184,15 @@ __device__ __forceinline__ void fill_dir_table(const Tabs& S) {
 }
 
 // One work item: the 8 centres of tile word w (column w+1) in row r.
-// RES = the resident kernel's layout (whole replica in shared memory, wrapped
-// copies in guard rows/words): only owned centres flip, and a flip that lands
-// on a copy is applied to the true site instead (copies are rebuilt after
-// every iteration).
+// MODE 0 = tile kernel.  MODE 1 = the resident kernel's layout (whole replica
+// in shared memory, wrapped copies in guard rows/words): only owned centres
+// flip, and a flip that lands on a copy is applied to the true site instead
+// (copies are rebuilt after every iteration).  MODE 2 = the band kernel: x as
+// in MODE 1, rows contiguous (halo rows are copies refreshed from the
+// neighbouring bands, flips landing there are recomputed by their owner).
 // FAST = every word of the tile is an aligned octet (checked per CTA), so the
 // per-centre draw path is compiled out and the item is one basic block.
-template <int KX, bool RES = false, bool FAST = false>
+template <int KX, int MODE = 0, bool FAST = false>
 __device__ __forceinline__ void process_item(const Tabs& S, int r, int w, uint32_t sweep, uint32_t c3,
                                              const uint32_t* rk, Acc& acc) {
     const uint32_t rl = kk_smem[S.rl_off + r];
@@ -298,7 +300,7 @@ __device__ __forceinline__ void process_item(const Tabs& S, int r, int w, uint32
     }
     uint32_t AN = accb & Dsel;
     uint32_t wm = 0;
-    if constexpr (RES) {
+    if constexpr (MODE != 0) {
         wm = (kk_smem[S.wm_off + w] >> KX) & kNib;
         AN &= wm;
     }
@@ -321,10 +323,12 @@ __device__ __forceinline__ void process_item(const Tabs& S, int r, int w, uint32
     int ro_u = ro + S.WS, ro_d = ro - S.WS;
     int nxt = 1, prv = -1;                    // word offsets of the right / left carries
     uint32_t prv_bit = 0x80000000u;
-    if constexpr (RES) {
+    if constexpr (MODE == 1) {
         // periodic rows: real rows are 2..rRows+1
         if (r == S.rRows + 1) ro_u -= S.rRows * S.WS;
         if (r == 2) ro_d += S.rRows * S.WS;
+    }
+    if constexpr (MODE != 0) {
         if (w == S.rW) {
             if (S.rTail) {  // bits >= Lx % 32 of the last word are copies of x = 0.. (tile word 1)
                 const uint32_t ov = 0xFFFFFFFFu << S.rTail;
@@ -358,8 +362,10 @@ __device__ __forceinline__ void process_item(const Tabs& S, int r, int w, uint32
 
     // ---- counters over owned centres (branch-free; in_mask = 0 for halo)
     uint32_t in_mask;
-    if constexpr (RES) {
+    if constexpr (MODE == 1) {
         in_mask = wm;
+    } else if constexpr (MODE == 2) {
+        in_mask = (rl >> 31) ? wm : 0u;
     } else {
         in_mask = (rl >> 31) ? ((kk_smem[S.wm_off + w] >> KX) & kNib) : 0u;
     }
@@ -382,7 +388,7 @@ __device__ __forceinline__ void run_iteration(const Tabs& S, int Wt, int r_first
     const int da = kThreads / Wt, dw = kThreads - da * Wt;
     int since_flush = 0;
     for (int it = threadIdx.x; it < items; it += kThreads) {
-        process_item<KX, false, FAST>(S, r_first + 4 * a, w, sweep, c3, rk, acc);
+        process_item<KX, 0, FAST>(S, r_first + 4 * a, w, sweep, c3, rk, acc);
         if (++since_flush == 32) {
             acc_flush(acc);
             since_flush = 0;
@@ -641,7 +647,7 @@ __device__ __forceinline__ void res_iteration(const Tabs& S, int r_first, uint32
     const int da = NT / W, dw = NT - da * W;
     int since_flush = 0;
     for (int it = threadIdx.x; it < items; it += NT) {
-        process_item<KX, true, true>(S, r_first + 4 * a, w + 1, sweep, c3, rk, acc);
+        process_item<KX, 1, true>(S, r_first + 4 * a, w + 1, sweep, c3, rk, acc);
         if (++since_flush == 32) {
             acc_flush(acc);
             since_flush = 0;
@@ -773,6 +779,238 @@ __global__ void __launch_bounds__(NT, 1024 / NT) resident_kernel(const ResParams
     }
 }
 
+
+// ---- band kernel -----------------------------------------------------------------
+// Mid-size lattices (too big for one SM, too small to fill the GPU with tiles
+// without heavy halo recomputation, e.g. 4096^2): the lattice is cut into
+// `nbands` row bands, one co-resident CTA each (cooperative launch), and stays
+// in shared memory for every iteration of a kk_sweep call.  After each
+// iteration a band publishes its first and last 3 rows to an L2 exchange
+// buffer, raises its flag (release), waits for both neighbours' flags
+// (acquire) and copies their rows into its 3-row halos.  Centres in the rows
+// just outside the band are processed redundantly by both neighbours (same
+// draws, same inputs: R8 with T = 1), so no flip ever crosses a band; flips
+// that land in a halo row are simply overwritten by the next exchange.
+// Shared layout as the resident kernel's, with local row lr = y - y0 + 3.
+
+__device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p) {
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release(unsigned int* p, unsigned int v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__host__ __device__ __forceinline__ int band_y0(int64_t rows, int nbands, int b) {
+    return (int)(4 * (((int64_t)b * (rows / 4)) / nbands));
+}
+
+template <int NT>
+__device__ __forceinline__ void band_refresh(const Tabs& S, int H) {
+    const int W = S.rW, tail = S.rTail, WS = S.WS;
+    const int nx = tail ? 3 : 2;  // rewritten words of every row: 0, W+1 (and W)
+    for (int i = threadIdx.x; i < H * nx; i += NT) {
+        const int r = i / nx, k = i - r * nx;
+        const int w = k == 0 ? 0 : (k == 1 ? W + 1 : W);
+        kk_smem[r * WS + kCol0 + w] = res_word(r * WS + kCol0, w, W, tail);
+    }
+}
+
+// Items of the centre rows r1 + 4a (a < n1) and r2 + 4a (a < n2).
+template <int KX, int NT>
+__device__ __forceinline__ void band_iteration(const Tabs& S, int r1, int n1, int r2, int n2, uint32_t sweep,
+                                               uint32_t c3, const uint32_t* rk, Acc& acc) {
+    const int W = S.rW;
+    const int items = (n1 + n2) * W;
+    int a = threadIdx.x / W;
+    int w = threadIdx.x - a * W;
+    const int da = NT / W, dw = NT - da * W;
+    int since_flush = 0;
+    for (int it = threadIdx.x; it < items; it += NT) {
+        const int r = a < n1 ? r1 + 4 * a : r2 + 4 * (a - n1);
+        process_item<KX, 2, true>(S, r, w + 1, sweep, c3, rk, acc);
+        if (++since_flush == 32) {
+            acc_flush(acc);
+            since_flush = 0;
+        }
+        a += da;
+        w += dw;
+        if (w >= W) {
+            w -= W;
+            ++a;
+        }
+    }
+}
+
+// centre rows of class ky among local rows [lo, hi): first row and count
+__device__ __forceinline__ void class_rows(int ky, int lo, int hi, int& first, int& n) {
+    // local row r holds y = y0 - 3 + r with y0 = 0 (mod 4): centre rows r = ky + 3 (mod 4)
+    first = lo + ((ky + 3 - lo) & 3);
+    n = hi > first ? (hi - first + 3) / 4 : 0;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT, 1) band_kernel(const BandParams P) {
+    const int b = blockIdx.x, nb = P.nbands;
+    const Geom& g = P.g;
+    const int W = g.W, tail = g.tail;
+    const int y0 = band_y0(g.rows, nb, b), y1 = band_y0(g.rows, nb, b + 1);
+    const int BR = y1 - y0, H = BR + 6, Wt = W + 2, WS = Wt + kCol0;
+    const int up = b == 0 ? nb - 1 : b - 1, dn = b + 1 == nb ? 0 : b + 1;
+    Tabs S;
+    S.WS = WS;
+    S.Lx = (uint32_t)g.Lx;
+    S.rW = W;
+    S.rTail = tail;
+    S.rRows = BR;
+    S.mt_off = P.mt_off;
+    S.wm_off = P.wm_off;
+    S.rl_off = P.rl_off;
+    S.th_off = P.th_off;
+    S.dt_off = P.dt_off;
+    unsigned long long* red = reinterpret_cast<unsigned long long*>(kk_smem + P.red_off);
+    uint2* thr2 = reinterpret_cast<uint2*>(kk_smem + S.th_off);
+    uint2* mtab = reinterpret_cast<uint2*>(kk_smem + S.mt_off);
+    for (int i = threadIdx.x; i < 256; i += NT) thr2[i] = make_uint2(P.thr[min(i & 15, 6)], P.thr[min(i >> 4, 6)]);
+    fill_dir_table<NT>(S);
+    for (int w = threadIdx.x; w < Wt; w += NT) {
+        mtab[w] = make_uint2(w >= 1 ? 32u * (uint32_t)(w - 1) : 0u, 1u);
+        uint32_t own = 0;
+        if (w >= 1 && w <= W) own = (w == W && tail) ? ((1u << tail) - 1u) : 0xFFFFFFFFu;
+        kk_smem[S.wm_off + w] = own;
+    }
+    for (int r = threadIdx.x; r < H; r += NT) {
+        const int64_t y = wrap_mod((int64_t)y0 - 3 + r, g.rows);
+        kk_smem[S.rl_off + r] = (uint32_t)(y >> 2) | ((r >= 3 && r < 3 + BR) ? 0x80000000u : 0u);
+    }
+    // stage the band and its halo rows (real words)
+    for (int i = threadIdx.x; i < H * W; i += NT) {
+        const int r = i / W, x = i - r * W;
+        const int64_t y = wrap_mod((int64_t)y0 - 3 + r, g.rows);
+        kk_smem[r * WS + kCol0 + 1 + x] = P.src[y * W + x];
+    }
+    __syncthreads();
+    band_refresh<NT>(S, H);
+    __syncthreads();
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0)
+        for (int k = 0; k < 4; ++k) red[k * (NT / 32) + warp] = 0ull;
+    Acc acc = {0u, 0u, 0u, 0u, 0u, 0ull};
+    uint32_t sweep = P.sweep0;
+    int j = P.j0;
+    int64_t left = P.n_iters;
+    unsigned int gi = 0;  // iterations published
+    const int64_t xrow = (int64_t)W;                 // words per exchanged row
+    const int64_t xside = 3 * xrow, xslot = 2 * xside, xband = 2 * xslot;
+#pragma unroll 1
+    while (left > 0) {
+        const Words4 sched = philox10(0u, 0u, sweep, kTagSchedule, P.key0, P.key1);
+        const int jend = (int)min64(16, j + left);
+        left -= jend - j;
+#pragma unroll 1
+        for (; j < jend; ++j) {
+            const uint32_t k = ((j < 8 ? sched.a : sched.b) >> (4 * (j & 7))) & 15u;
+            const int kx = (int)(k & 3u), ky = (int)(k >> 2);
+            const uint32_t c3 = (uint32_t)j;
+            // Centre rows [2, BR + 4).  Boundary rows (within 2 of a published
+            // row's writers: [2, 7) and [BR - 1, BR + 4)) first; then publish;
+            // then the interior rows [7, BR - 1) while the exchange is in flight.
+            const int bt_hi = min(7, BR + 4), bb_lo = max(bt_hi, BR - 1);
+            int rt, nt_, rb, nb_, ri, ni;
+            class_rows(ky, 2, bt_hi, rt, nt_);
+            class_rows(ky, bb_lo, BR + 4, rb, nb_);
+            class_rows(ky, bt_hi, bb_lo, ri, ni);
+#define KK_BAND_ITEMS(R1, N1, R2, N2)                                                             \
+    switch (kx) {                                                                                 \
+        case 0: band_iteration<0, NT>(S, R1, N1, R2, N2, sweep, c3, P.rk, acc); break;           \
+        case 1: band_iteration<1, NT>(S, R1, N1, R2, N2, sweep, c3, P.rk, acc); break;           \
+        case 2: band_iteration<2, NT>(S, R1, N1, R2, N2, sweep, c3, P.rk, acc); break;           \
+        default: band_iteration<3, NT>(S, R1, N1, R2, N2, sweep, c3, P.rk, acc); break;          \
+    }
+            KK_BAND_ITEMS(rt, nt_, rb, nb_)
+            __syncthreads();
+            // publish: side 0 = first 3 real rows, side 1 = last 3
+            ++gi;
+            const int slot = (int)(gi & 1u);
+            uint32_t* xo = P.xch + (int64_t)b * xband + slot * xslot;
+            for (int i = threadIdx.x; i < 6 * W; i += NT) {
+                const int k6 = i / W, x = i - k6 * W;
+                const int lr = k6 < 3 ? 3 + k6 : BR + k6 - 3;
+                xo[(k6 < 3 ? 0 : xside) + (k6 % 3) * xrow + x] = kk_smem[lr * WS + kCol0 + 1 + x];
+            }
+            __syncthreads();
+            // the barrier orders the CTA's stores before thread 0's release
+            // (cumulative), which orders them before the flag
+            if (threadIdx.x == 0) st_release(P.flags + b, gi);
+            KK_BAND_ITEMS(ri, ni, 0, 0)
+            acc_flush(acc);
+            if (threadIdx.x == 0) {
+                long long spins = 0;
+                while (ld_acquire(P.flags + up) < gi || ld_acquire(P.flags + dn) < gi) {
+                    if (++spins > (1ll << 28)) {  // a neighbour never arrived: give up loudly
+                        atomicExch(P.error, 1u);
+                        break;
+                    }
+                }
+            }
+            __syncthreads();
+            // halos: rows y0-3..y0-1 = up's last 3 rows, y1..y1+2 = dn's first 3 rows
+            const uint32_t* xu = P.xch + (int64_t)up * xband + slot * xslot + xside;
+            const uint32_t* xd = P.xch + (int64_t)dn * xband + slot * xslot;
+            for (int i = threadIdx.x; i < 6 * W; i += NT) {
+                const int k6 = i / W, x = i - k6 * W;
+                const int lr = k6 < 3 ? k6 : BR + k6;  // 0..2 and BR+3..BR+5
+                const uint32_t* src = k6 < 3 ? xu : xd;
+                kk_smem[lr * WS + kCol0 + 1 + x] = __ldcg(src + (k6 % 3) * xrow + x);
+            }
+            __syncthreads();
+            band_refresh<NT>(S, H);
+            __syncthreads();
+#undef KK_BAND_ITEMS
+        }
+        if (j == 16) {
+            j = 0;
+            ++sweep;
+        }
+        uint32_t c0 = acc.attempted, c1 = acc.trivial, c2 = acc.accepted, c3s = (uint32_t)acc.idx_sum;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            c0 += __shfl_xor_sync(0xFFFFFFFFu, c0, o);
+            c1 += __shfl_xor_sync(0xFFFFFFFFu, c1, o);
+            c2 += __shfl_xor_sync(0xFFFFFFFFu, c2, o);
+            c3s += __shfl_xor_sync(0xFFFFFFFFu, c3s, o);
+        }
+        if (lane == 0) {
+            red[0 * (NT / 32) + warp] += c0;
+            red[1 * (NT / 32) + warp] += c1;
+            red[2 * (NT / 32) + warp] += c2;
+            red[3 * (NT / 32) + warp] += c3s;
+        }
+        acc.attempted = acc.trivial = acc.accepted = 0u;
+        acc.idx_sum = 0ull;
+    }
+
+    // write back the band's real words
+    const uint32_t last = tail ? ((1u << tail) - 1u) : 0xFFFFFFFFu;
+    for (int i = threadIdx.x; i < BR * W; i += NT) {
+        const int r = i / W, x = i - r * W;
+        const uint32_t v = kk_smem[(r + 3) * WS + kCol0 + 1 + x];
+        P.dst[(int64_t)(y0 + r) * W + x] = x == W - 1 ? (v & last) : v;
+    }
+    if (lane == 0)
+        red[3 * (NT / 32) + warp] =
+            (unsigned long long)(2 * ((long long)red[3 * (NT / 32) + warp] - 3 * (long long)red[2 * (NT / 32) + warp]));
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        unsigned long long s = 0;
+        for (int k = 0; k < NT / 32; ++k) s += red[threadIdx.x * (NT / 32) + k];
+        if (s) atomicAdd(P.stats + threadIdx.x, s);
+    }
+}
+
 }  // namespace
 
 int pass_smem_bytes(int T, int THI, int TWI) {
@@ -840,6 +1078,52 @@ cudaError_t launch_resident(const ResParams& P, int64_t replicas, int nt, cudaSt
             return cudaErrorInvalidValue;
     }
 #undef KK_RES
+    count_launch();
+    return cudaGetLastError();
+}
+
+// Band kernel geometry: 1024-thread CTAs, one per SM; 0 if the lattice does
+// not qualify (full periodic lattice, one replica, Lx >= 64 and W >= 3 with a
+// tail, every band >= 4 rows and within shared memory).
+constexpr int kBandThreads = 1024;
+
+int band_smem_bytes(const Geom& g, int nbands) {
+    if (g.Lx < 64 || (g.tail && g.W < 3) || !g.periodic || nbands < 2 || g.rows / 4 < nbands) return 0;
+    int max_rows = 0;
+    for (int b = 0; b < nbands; ++b) max_rows = std::max(max_rows, band_y0(g.rows, nbands, b + 1) - band_y0(g.rows, nbands, b));
+    const int64_t H = max_rows + 6, Wt = g.W + 2, WS = Wt + kCol0;
+    if (H * WS > 227 * 256) return 0;
+    const int64_t bytes = 4 * (int64_t)smem_layout((int)H, (int)Wt, (int)WS).words;
+    return bytes <= 227 * 1024 ? (int)bytes : 0;
+}
+
+void set_band_layout(BandParams& P) {
+    int max_rows = 0;
+    for (int b = 0; b < P.nbands; ++b)
+        max_rows = std::max(max_rows, band_y0(P.g.rows, P.nbands, b + 1) - band_y0(P.g.rows, P.nbands, b));
+    P.max_rows = max_rows;
+    const SmemLayout L = smem_layout(max_rows + 6, P.g.W + 2, P.g.W + 2 + kCol0);
+    P.mt_off = L.mt_off;
+    P.wm_off = L.wm_off;
+    P.rl_off = L.rl_off;
+    P.th_off = L.th_off;
+    P.dt_off = L.dt_off;
+    P.red_off = L.red_off;
+}
+
+int64_t band_xch_words(const Geom& g, int nbands) { return (int64_t)nbands * 2 * 2 * 3 * g.W; }
+
+cudaError_t launch_band(const BandParams& P, cudaStream_t stream) {
+    const int smem = band_smem_bytes(P.g, P.nbands);
+    if (!smem) return cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(band_kernel<kBandThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(P.flags, 0, sizeof(unsigned int) * P.nbands, stream);
+    if (e != cudaSuccess) return e;
+    void* args[] = {const_cast<BandParams*>(&P)};
+    e = cudaLaunchCooperativeKernel((const void*)band_kernel<kBandThreads>, dim3((unsigned)P.nbands),
+                                    dim3(kBandThreads), args, (size_t)smem, stream);
+    if (e != cudaSuccess) return e;
     count_launch();
     return cudaGetLastError();
 }

@@ -95,3 +95,43 @@ def test_config3_replica_batch_sample():
 def test_resident_cta_sizes(Lx, Ly, R, nt):
     """All resident CTA sizes (KK_RES_THREADS) give the oracle's result."""
     _run_parity(Lx, Ly, 0.4, 0.8, 5 + nt, 4, R=R, env={"KK_RESIDENT": 2, "KK_RES_THREADS": nt})
+
+
+# ---- band kernel (lattice spread over all SMs' shared memory, 3-row halo
+# exchange between neighbouring bands through L2 every iteration)
+@pytest.mark.parametrize("Lx,Ly", [(64, 64), (100, 40), (68, 16), (400, 400), (1000, 44), (2048, 64),
+                                   (4096, 600)])
+def test_band_kernel_matches_oracle(Lx, Ly):
+    _run_parity(Lx, Ly, 0.5, 0.7, Lx + 3 * Ly, 4, env={"KK_RESIDENT": 0, "KK_BAND": 2})
+
+
+def test_band_kernel_mid_sweep_start_and_omega():
+    from paper_1309_4349_b200 import kk
+    Lx, Ly, seed, om = 2048, 96, 99, 1.1
+    L = _lat(Lx, Ly, 0.4, om, seed, iters_per_pass=4, env={"KK_RESIDENT": 0, "KK_BAND": 2})
+    ref = O.init_random(Lx, Ly, 0.4, seed)
+    L.run_pass(kk.REGION_ALL, None, None)      # tile kernel: iterations 0..3 of sweep 0
+    L.pass_commit()
+    L.sweep(2)                                  # band kernel from (sweep 0, j = 4)
+    for _ in range(3):
+        L.run_pass(kk.REGION_ALL, None, None)
+        L.pass_commit()
+    ost = O.run(ref, om, seed, 3)
+    assert np.array_equal(L.get_lattice()[0], ref)
+    assert list(L.stats()[0]) == [ost["attempted"], ost["trivial"], ost["accepted"], ost["dnab_sum"]]
+
+
+def test_config2_4096_band_and_tile_agree():
+    """BASELINE configs[2] (4096^2): the band kernel (KK_BAND=2, opt-in) and
+    the default tile kernel give the identical lattice and counters, equal to
+    the oracle's."""
+    from paper_1309_4349_b200 import kk
+    A = _lat(4096, 4096, 0.5, 0.6, 4096, init=kk.KK_INIT_RANDOM, env={"KK_BAND": 2})
+    B = _lat(4096, 4096, 0.5, 0.6, 4096, init=kk.KK_INIT_RANDOM)
+    A.sweep(3)
+    B.sweep(3)
+    assert np.array_equal(A.get_packed(), B.get_packed())
+    assert np.array_equal(A.stats(), B.stats())
+    ref = O.init_random(4096, 4096, 0.5, 4096)
+    O.run(ref, 0.6, 4096, 3)
+    assert np.array_equal(A.get_lattice()[0], ref)
