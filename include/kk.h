@@ -87,8 +87,15 @@ int kk_destroy(kk_handle h);
 /* Run n MPKK sweeps (n Monte Carlo steps; R4): each sweep
  * is 16 iterations; iteration j draws a centre class k_j (R6) and performs one
  * Kawasaki exchange attempt per centre.  Sweep indices continue from the
- * handle's sweep counter.  Only for full-lattice handles (KK_ERR_STATE on a
- * slab).  Asynchronous on `stream`. */
+ * handle's sweep counter (and iteration, if kk_pass left it mid-sweep).  Only
+ * for full-lattice handles (KK_ERR_STATE on a slab).  Asynchronous on
+ * `stream`.  The kernel is chosen at kk_create time and never changes the
+ * result (every path is bit-identical): replicas that fit in one
+ * SM's shared memory run the resident kernel (all n sweeps in one launch),
+ * larger lattices the tile kernel (16/T launches per sweep);
+ * environment overrides for testing: KK_RESIDENT=0/2 (never/always when it
+ * fits), KK_BAND=2 (band kernel), KK_THI/KK_TWI (tile shape),
+ * KK_RES_THREADS=128/256/512. */
 int kk_sweep(kk_handle h, int64_t n, void* stream);
 
 /* Energy per replica (R3): nab_out[r] = N_AB (unlike nearest-neighbour pairs,
