@@ -8,6 +8,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -15,12 +17,27 @@
 #include <cudaTypedefs.h>
 
 #include "../../include/kk.h"
+
 #include "kk_internal.cuh"
 
 namespace kk {
 
 static std::atomic<long long> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+cudaError_t ensure_dynamic_smem(const void* fn, int bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, int> granted;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    int& g = granted[{dev, fn}];
+    if (bytes <= g) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) g = bytes;
+    return e;
+}
 
 int pass_smem_bytes(int T, int THI, int TWI);
 void set_pass_layout(int T, PassParams& P);
@@ -506,8 +523,13 @@ int kk_create_ex(kk_handle* out, const kk_config* c) {
         int nsm = 148;
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device);
         if (nsm <= 0) nsm = 148;
+        // small replicas (<= 512^2 sites) always: one launch per kk_sweep call
+        // and one SM per replica, so independent handles on separate streams
+        // run side by side (18 x 400^2 handles: 33 G/s resident vs 4 G/s for
+        // launch-bound tile passes, tools/single_small.py)
+        const bool small = h->g.Lx * h->g.rows <= 512 * 512;
         h->resident = resident_smem_bytes(h->g) > 0 &&
-                              (mode == 2 || (mode == 1 && (tile_ctas <= 2 || h->R >= nsm)))
+                              (mode == 2 || (mode == 1 && (tile_ctas <= 2 || h->R >= nsm || small)))
                           ? 1
                           : 0;
         h->res_nt = resident_threads(h->g, h->R, nsm, env_int("KK_RES_THREADS", 0));

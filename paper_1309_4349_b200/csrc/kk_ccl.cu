@@ -478,7 +478,7 @@ cudaError_t launch_ccl(const uint32_t* lat, const Geom& g, int64_t replicas, int
     cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(unsigned int), s);
     if (e != cudaSuccess) return e;
     const int smem = 4 * (2 * kTR * kTW + kSites / 32 + kSites + kSites / 2) + 2 * kEdge;
-    e = cudaFuncSetAttribute(ccl_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    e = ensure_dynamic_smem((const void*)ccl_tile_kernel, smem);
     if (e != cudaSuccess) return e;
     ccl_tile_kernel<<<dim3(P.tiles_x, P.tiles_y, (unsigned)replicas), kThreads, smem, s>>>(P);
     count_launch();

@@ -220,4 +220,11 @@ struct SlabCclArgs {
 // ---------------------------------------------------------------- launch counter
 void count_launch();
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) only when a kernel needs
+// more than it was last granted on this device: changing a function attribute
+// can serialise it against launches in flight on other streams (measured:
+// 18 handles on 18 streams ran one at a time), so steady-state launches must
+// not touch it.  kk_api.cu.
+cudaError_t ensure_dynamic_smem(const void* fn, int bytes);
+
 }  // namespace kk

@@ -1066,7 +1066,7 @@ cudaError_t launch_resident(const ResParams& P, int64_t replicas, int nt, cudaSt
     cudaError_t e = cudaSuccess;
 #define KK_RES(NTT)                                                                                    \
     case NTT:                                                                                          \
-        e = cudaFuncSetAttribute(resident_kernel<NTT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+        e = ensure_dynamic_smem((const void*)resident_kernel<NTT>, smem); \
         if (e != cudaSuccess) return e;                                                                \
         resident_kernel<NTT><<<(unsigned)replicas, NTT, smem, stream>>>(P);                            \
         break;
@@ -1116,7 +1116,7 @@ int64_t band_xch_words(const Geom& g, int nbands) { return (int64_t)nbands * 2 *
 cudaError_t launch_band(const BandParams& P, cudaStream_t stream) {
     const int smem = band_smem_bytes(P.g, P.nbands);
     if (!smem) return cudaErrorInvalidValue;
-    cudaError_t e = cudaFuncSetAttribute(band_kernel<kBandThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = ensure_dynamic_smem((const void*)band_kernel<kBandThreads>, smem);
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(P.flags, 0, sizeof(unsigned int) * P.nbands, stream);
     if (e != cudaSuccess) return e;
@@ -1137,11 +1137,11 @@ cudaError_t launch_pass(int T, const PassParams& P, const CUtensorMap& tmap, int
 #define KK_LAUNCH(TT)                                                                                  \
     case TT:                                                                                           \
         if (P.g.tail == 0) {                                                                           \
-            e = cudaFuncSetAttribute(pass_kernel<TT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+            e = ensure_dynamic_smem((const void*)pass_kernel<TT, true>, smem); \
             if (e != cudaSuccess) return e;                                                            \
             pass_kernel<TT, true><<<grid, kThreads, smem, stream>>>(tmap, P);                          \
         } else {                                                                                       \
-            e = cudaFuncSetAttribute(pass_kernel<TT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+            e = ensure_dynamic_smem((const void*)pass_kernel<TT, false>, smem); \
             if (e != cudaSuccess) return e;                                                            \
             pass_kernel<TT, false><<<grid, kThreads, smem, stream>>>(tmap, P);                         \
         }                                                                                              \
