@@ -520,10 +520,28 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
         const uint32_t k = ((j < 8 ? sched.a : sched.b) >> (4 * (j & 7))) & 15u;
         const int kx = (int)(k & 3u), ky = (int)(k >> 2);
         const uint32_t c3 = ((uint32_t)rep << 8) | (uint32_t)j;
-        // rows whose centres can still influence the interior (light cone)
-        const int ext = 3 * (T - 1 - t) + 1;
-        const int r_lo = max(2, HY - ext);
-        const int r_hi = min(H - 2, HY + P.THI + ext);
+        // Rows whose centres can still influence the interior (light cone,
+        // R8), from the actual classes of the remaining iterations: walking
+        // back from [HY, HY + THI), iteration u needs its centre rows c in
+        // [a - 1, b + 1) and their reads [c - 2, c + 2], so the exact range
+        // grows by 0..3 rows per iteration (1.5 on average) instead of the
+        // worst-case 3 that sizes the staged halo.
+        int a = HY, b = HY + P.THI;
+#pragma unroll
+        for (int u = T - 1; u > 0; --u) {
+            if (u <= t) break;
+            const int ju = P.j0 + u;
+            const int kyu = (int)((((ju < 8 ? sched.a : sched.b) >> (4 * (ju & 7))) & 15u) >> 2);
+            const int ph = (kyu - phase0) & 3;
+            const int cmin = (a - 1) + ((ph - (a - 1)) & 3);
+            const int cmax = b - ((b - ph) & 3);
+            if (cmin <= cmax) {
+                a = min(a, cmin - 2);
+                b = max(b, cmax + 3);
+            }
+        }
+        const int r_lo = max(2, a - 1);
+        const int r_hi = min(H - 2, b + 1);
         const int phase = (ky - phase0) & 3;  // active rows: r = phase (mod 4)
         const int r_first = r_lo + ((phase - r_lo) & 3);
         const int nrows = r_hi > r_first ? (r_hi - r_first + 3) / 4 : 0;
