@@ -1,19 +1,29 @@
-// kk_pass.cu — the MPKK hot loop: T iterations of a sweep per HBM pass.
+// kk_pass.cu — the MPKK hot loop.
 //
 // PAPER.md:104-114 (MPKK listing): iteration j of sweep s picks a centre
 // class k_j and performs one Kawasaki exchange attempt per centre; here the
 // 16 classes are {x = kx, y = ky (mod 4)} (R4), so all centres of an
 // iteration are independent and are processed concurrently.
 //
-// Tile design (sm_100a): a CTA owns an interior of THI rows x TWI words
-// (32*TWI sites) of one replica and stages it in shared memory with HY = 3T
-// halo rows and one halo word per side (R8: after T iterations the
-// interior is exact).  The T iterations run entirely in shared memory; the
-// lattice crosses HBM once per T iterations (read tile+halo, write the
-// interior to the other buffer).  Everything that depends only on the tile
-// position (global centre-pair indices per word, centre-row indices per row,
-// ownership masks) is tabulated in shared memory once per pass, so the inner
-// loop is pure 32-bit integer work.
+// Three kernels share one work-item routine (process_item) and differ only in
+// where the lattice lives between iterations:
+//  * pass_kernel<T>: large lattices.  A CTA owns an interior of THI rows x TWI
+//    words of one replica and stages it in shared memory with HY = 3T halo
+//    rows and one halo word per side (R8: after T iterations the
+//    interior is exact; the rows actually processed follow the exact light
+//    cone of the pass's classes).  The lattice crosses HBM once per T
+//    iterations (read tile+halo, write the interior to the other buffer).
+//  * resident_kernel<NT>: replicas that fit in one SM's shared memory; one
+//    CTA per replica runs every iteration of a kk_sweep call in place, the
+//    periodic wrap kept as rebuilt copies.
+//  * band_kernel<NT> (opt-in): one row band per SM, the whole lattice in
+//    shared memory across the GPU, 3-row halos exchanged through L2 per
+//    iteration.
+// Everything that depends only on the tile position (global centre-octet
+// indices per word, centre-row indices per row, ownership masks) and the
+// per-pass constants (pair threshold table, pair direction table) is
+// tabulated in shared memory once per launch, so the inner loop is pure
+// 32-bit integer work.
 //
 // Work item = (row of the active class, 32-bit word): 8 centres.  The energy
 // change of all six possible exchanges of all 8 centres is computed with
