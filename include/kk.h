@@ -82,6 +82,27 @@ int kk_create(kk_handle* out, int64_t Lx, int64_t Ly, double fraction_A,
  * (kk_pass); a handle with y_count == Ly is periodic by itself. */
 int kk_create_ex(kk_handle* out, const kk_config* cfg);
 
+/* The execution plan kk_create_ex would choose for `cfg` (host logic only:
+ * no allocation, no kernel; no CUDA call at all when n_sm > 0, so it can be
+ * inspected and tested without a GPU).  n_sm = SMs of the target device
+ * (<= 0: query cfg->device or the current device).  The plan never changes
+ * results (every kernel is bit-identical); it decides speed.
+ * Honours the same environment overrides as kk_create_ex (kk_sweep). */
+enum { KK_KERNEL_TILE = 0, KK_KERNEL_RESIDENT = 1, KK_KERNEL_BAND = 2 };
+typedef struct {
+    int32_t kernel;          /* KK_KERNEL_*: what kk_sweep launches */
+    int32_t iters_per_pass;  /* T of the tile kernel (kk_pass always uses the tile kernel) */
+    int32_t tile_rows;       /* tile kernel: interior rows per CTA (THI, multiple of 4) */
+    int32_t tile_words;      /* tile kernel: interior 32-bit words per CTA row (TWI) */
+    int32_t tiles_x, bands;  /* tile kernel: tiles per row, row bands per replica */
+    int32_t halo_rows;       /* 3*T: halo rows a slab pass needs from each neighbour (R8) */
+    int32_t threads;         /* CTA size of the chosen kernel */
+    int32_t smem_bytes;      /* dynamic shared memory per CTA of the chosen kernel */
+    int32_t reserved;
+    int64_t ctas;            /* CTAs per launch of the chosen kernel */
+} kk_plan;
+int kk_plan_config(const kk_config* cfg, int n_sm, kk_plan* out);
+
 int kk_destroy(kk_handle h);
 
 /* Run n MPKK sweeps (n Monte Carlo steps; R4): each sweep

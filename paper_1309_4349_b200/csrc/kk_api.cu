@@ -194,14 +194,11 @@ void set_tiles(kk_lattice* h, int twi_t, int thi_t) {
     h->bands = (int)((rows + thi - 1) / thi);
 }
 
-void choose_tiles(kk_lattice* h) {
+void choose_tiles(kk_lattice* h, int nsm) {
     const int twi_env = env_int("KK_TWI", 0), thi_env = env_int("KK_THI", 0);
     if (twi_env > 0 || thi_env > 0) {
         set_tiles(h, std::max(1, twi_env > 0 ? twi_env : 64), std::max(4, thi_env > 0 ? thi_env : 320));
     } else {
-        int nsm = 148;
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device);
-        if (nsm <= 0) nsm = 148;
         const int T = h->T;
         double best = 1e300;
         int bt = 64, bh = 320;
@@ -470,9 +467,13 @@ const char* kk_last_error(void) { return g_err.c_str(); }
 const char* kk_version(void) { return "kk 0.1 (sm_100a, MPKK 4x4 centre classes, Philox4x32-10)"; }
 int64_t kk_launch_count(void) { return (int64_t)g_launches.load(); }
 
-int kk_create_ex(kk_handle* out, const kk_config* c) {
-    if (!out || !c) return fail(KK_ERR_ARG, "null argument");
-    *out = nullptr;
+}  // extern "C"
+
+namespace {
+
+// Argument checks of kk_create_ex / kk_plan_config (no CUDA calls).
+int validate_config(const kk_config* c, int* T_out) {
+    if (!c) return fail(KK_ERR_ARG, "null argument");
     if (c->Lx < 4 || c->Lx % 4) return fail(KK_ERR_ARG, "Lx must be a positive multiple of 4 (DESIGN.md R10)");
     if (c->Ly < 4 || c->Ly % 4) return fail(KK_ERR_ARG, "Ly must be a positive multiple of 4 (DESIGN.md R10)");
     if (c->y_count < 4 || c->y_count % 4 || c->y_begin < 0 || c->y_begin % 4 || c->y_begin + c->y_count > c->Ly)
@@ -487,6 +488,113 @@ int kk_create_ex(kk_handle* out, const kk_config* c) {
     if (slab && c->y_count < 3 * T) return fail(KK_ERR_ARG, "slab must hold at least 3*T rows (halo depth)");
     if (slab && c->init_mode == KK_INIT_RANDOM)
         return fail(KK_ERR_ARG, "slab handles: random start needs the distributed selection (use KK_INIT_EMPTY)");
+    *T_out = T;
+    return KK_OK;
+}
+
+// Geometry and kernel choice (host logic only, no CUDA calls): tile shape,
+// resident / band kernel, resident CTA size.  nsm = SMs of the device.
+int plan_handle(kk_lattice* h, const kk_config* c, int T, int nsm) {
+    h->g.Lx = c->Lx;
+    h->g.W = (int32_t)((c->Lx + 31) / 32);
+    h->g.tail = (int32_t)(c->Lx % 32);
+    h->g.rows = c->y_count;
+    h->g.y_begin = c->y_begin;
+    h->g.Ly = c->Ly;
+    h->g.rep_words = c->y_count * h->g.W;
+    h->g.periodic = c->y_count != c->Ly ? 0 : 1;
+    h->R = c->replicas;
+    h->fraction_A = c->fraction_A;
+    h->omega = c->omega_kT;
+    h->seed = c->seed;
+    h->T = T;
+    h->hy = 3 * T;
+    make_thresholds(h->omega, h->thr);
+    choose_tiles(h, nsm);
+    // resident kernel: one CTA per replica, all sweeps of a kk_sweep call in
+    // one launch.  Auto (KK_RESIDENT=1, default) when the tile kernel would
+    // not spread a replica over more than two CTAs anyway, when there are
+    // enough replicas to fill every SM, or for small replicas (<= 512^2
+    // sites: one launch per kk_sweep call and one SM per replica, so
+    // independent handles on separate streams run side by side — 18 x 400^2
+    // handles: 33 G/s resident vs 4 G/s for launch-bound tile passes,
+    // tools/single_small.py); 2 = whenever the replica fits; 0 = never.
+    const int mode = env_int("KK_RESIDENT", 1);
+    const int64_t tile_ctas = (int64_t)h->tiles_x * h->bands;
+    const bool small = h->g.Lx * h->g.rows <= 512 * 512;
+    h->resident = resident_smem_bytes(h->g) > 0 &&
+                          (mode == 2 || (mode == 1 && (tile_ctas <= 2 || h->R >= nsm || small)))
+                      ? 1
+                      : 0;
+    h->res_nt = resident_threads(h->g, h->R, nsm, env_int("KK_RES_THREADS", 0));
+    // band kernel: one replica too big for one SM, spread over all SMs'
+    // shared memory.  Opt-in (KK_BAND=2): measured on B200 it loses to the
+    // tile kernel below ~8192^2 and wins only ~3% at 12288^2 (the L2
+    // handshake per iteration costs ~3 us, tools/band_vs_tile.py).
+    const int bmode = env_int("KK_BAND", 0);
+    const int nb = (int)std::min<int64_t>(nsm, h->g.rows / 4);
+    h->nbands = (!h->resident && h->R == 1 && bmode == 2 && band_smem_bytes(h->g, nb) > 0) ? nb : 0;
+    if (pass_smem_bytes(T, h->THI, h->TWI) > 227 * 1024)
+        return fail(KK_ERR_ARG, "tile too large for shared memory (KK_THI/KK_TWI)");
+    return KK_OK;
+}
+
+int device_sms(int device) {
+    int nsm = 0;
+    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || nsm <= 0) {
+        cudaGetLastError();
+        return 148;
+    }
+    return nsm;
+}
+
+}  // namespace
+
+extern "C" {
+
+int kk_plan_config(const kk_config* c, int n_sm, kk_plan* out) {
+    if (!out) return fail(KK_ERR_ARG, "null argument");
+    int T = 0;
+    int rc = validate_config(c, &T);
+    if (rc != KK_OK) return rc;
+    if (n_sm <= 0) {
+        int dev = c->device;
+        if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) return fail(KK_ERR_CUDA, "no CUDA device (pass n_sm)");
+        n_sm = device_sms(dev);
+    }
+    kk_lattice tmp;
+    rc = plan_handle(&tmp, c, T, n_sm);
+    if (rc != KK_OK) return rc;
+    *out = kk_plan{};
+    out->kernel = tmp.nbands ? KK_KERNEL_BAND : (tmp.resident ? KK_KERNEL_RESIDENT : KK_KERNEL_TILE);
+    out->iters_per_pass = T;
+    out->tile_rows = tmp.THI;
+    out->tile_words = tmp.TWI;
+    out->tiles_x = tmp.tiles_x;
+    out->bands = tmp.bands;
+    out->halo_rows = tmp.hy;
+    if (out->kernel == KK_KERNEL_TILE) {
+        out->threads = 512;
+        out->smem_bytes = pass_smem_bytes(T, tmp.THI, tmp.TWI);
+        out->ctas = (int64_t)tmp.tiles_x * tmp.bands * tmp.R;
+    } else if (out->kernel == KK_KERNEL_RESIDENT) {
+        out->threads = tmp.res_nt;
+        out->smem_bytes = resident_smem_bytes(tmp.g);
+        out->ctas = tmp.R;
+    } else {
+        out->threads = 1024;
+        out->smem_bytes = band_smem_bytes(tmp.g, tmp.nbands);
+        out->ctas = tmp.nbands;
+    }
+    return KK_OK;
+}
+
+int kk_create_ex(kk_handle* out, const kk_config* c) {
+    if (!out || !c) return fail(KK_ERR_ARG, "null argument");
+    *out = nullptr;
+    int T = 0;
+    int rc0 = validate_config(c, &T);
+    if (rc0 != KK_OK) return rc0;
 
     kk_lattice* h = new kk_lattice();
     h->device = c->device;
@@ -496,54 +604,10 @@ int kk_create_ex(kk_handle* out, const kk_config* c) {
     } else {
         cudaGetDevice(&h->device);
     }
-    h->g.Lx = c->Lx;
-    h->g.W = (int32_t)((c->Lx + 31) / 32);
-    h->g.tail = (int32_t)(c->Lx % 32);
-    h->g.rows = c->y_count;
-    h->g.y_begin = c->y_begin;
-    h->g.Ly = c->Ly;
-    h->g.rep_words = c->y_count * h->g.W;
-    h->g.periodic = slab ? 0 : 1;
-    h->R = c->replicas;
-    h->fraction_A = c->fraction_A;
-    h->omega = c->omega_kT;
-    h->seed = c->seed;
-    h->T = T;
-    h->hy = 3 * T;
-    make_thresholds(h->omega, h->thr);
-    choose_tiles(h);
-    {
-        // resident kernel: one CTA per replica, all sweeps of a kk_sweep call in
-        // one launch.  Auto (KK_RESIDENT=1, default) when the tile kernel would
-        // not spread a replica over more than two CTAs anyway, or when there
-        // are enough replicas to fill every SM; 2 = whenever the replica fits;
-        // 0 = never.
-        const int mode = env_int("KK_RESIDENT", 1);
-        const int64_t tile_ctas = (int64_t)h->tiles_x * h->bands;
-        int nsm = 148;
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device);
-        if (nsm <= 0) nsm = 148;
-        // small replicas (<= 512^2 sites) always: one launch per kk_sweep call
-        // and one SM per replica, so independent handles on separate streams
-        // run side by side (18 x 400^2 handles: 33 G/s resident vs 4 G/s for
-        // launch-bound tile passes, tools/single_small.py)
-        const bool small = h->g.Lx * h->g.rows <= 512 * 512;
-        h->resident = resident_smem_bytes(h->g) > 0 &&
-                              (mode == 2 || (mode == 1 && (tile_ctas <= 2 || h->R >= nsm || small)))
-                          ? 1
-                          : 0;
-        h->res_nt = resident_threads(h->g, h->R, nsm, env_int("KK_RES_THREADS", 0));
-        // band kernel: one replica too big for one SM, spread over all SMs'
-        // shared memory.  Opt-in (KK_BAND=2): measured on B200 it loses to the
-        // tile kernel below ~8192^2 and wins only ~3% at 12288^2 (the L2
-        // handshake per iteration costs ~3 us, tools/band_vs_tile.py).
-        const int bmode = env_int("KK_BAND", 0);
-        const int nb = (int)std::min<int64_t>(nsm, h->g.rows / 4);
-        if (!h->resident && h->R == 1 && bmode == 2 && band_smem_bytes(h->g, nb) > 0) h->nbands = nb;
-    }
-    if (pass_smem_bytes(T, h->THI, h->TWI) > 227 * 1024) {
+    rc0 = plan_handle(h, c, T, device_sms(h->device));
+    if (rc0 != KK_OK) {
         delete h;
-        return fail(KK_ERR_ARG, "tile too large for shared memory (KK_THI/KK_TWI)");
+        return rc0;
     }
     const size_t words = (size_t)h->R * (size_t)h->g.rep_words;
     cudaError_t e1 = cudaMalloc(&h->buf[0], words * 4);

@@ -36,10 +36,21 @@ class Config(ctypes.Structure):
                 ("reserved", ctypes.c_int32)]
 
 
+class Plan(ctypes.Structure):
+    _fields_ = [("kernel", ctypes.c_int32), ("iters_per_pass", ctypes.c_int32), ("tile_rows", ctypes.c_int32),
+                ("tile_words", ctypes.c_int32), ("tiles_x", ctypes.c_int32), ("bands", ctypes.c_int32),
+                ("halo_rows", ctypes.c_int32), ("threads", ctypes.c_int32), ("smem_bytes", ctypes.c_int32),
+                ("reserved", ctypes.c_int32), ("ctas", ctypes.c_int64)]
+
+
+KERNEL_NAMES = {0: "tile", 1: "resident", 2: "band"}
+
+
 # symbol -> (restype, argtypes); the ABI surface declared in include/kk.h
 SIGNATURES = {
     "kk_create": (ctypes.c_int, [ctypes.POINTER(_p), _i64, _i64, ctypes.c_double, ctypes.c_double, ctypes.c_uint64]),
     "kk_create_ex": (ctypes.c_int, [ctypes.POINTER(_p), ctypes.POINTER(Config)]),
+    "kk_plan_config": (ctypes.c_int, [ctypes.POINTER(Config), ctypes.c_int, ctypes.POINTER(Plan)]),
     "kk_destroy": (ctypes.c_int, [_p]),
     "kk_sweep": (ctypes.c_int, [_p, _i64, _p]),
     "kk_energy": (ctypes.c_int, [_p, _p, _p, _p, _p]),
@@ -121,6 +132,20 @@ def cluster_join(Lx: int, nslabs: int, top_ids: int, bot_ids: int, offsets, size
             continue
         _check(rc, "kk_cluster_join")
         return buf[: n.value]
+
+
+def plan(Lx: int, Ly: int, replicas: int = 1, iters_per_pass: int = 0, y_begin: int = 0,
+         y_count: Optional[int] = None, n_sm: int = 148, init: int = KK_INIT_EMPTY) -> dict:
+    """kk_plan_config: the kernel and launch shape kk_create would choose (no
+    GPU needed when n_sm > 0)."""
+    cfg = Config(Lx=Lx, Ly=Ly, y_begin=y_begin, y_count=Ly if y_count is None else y_count, replicas=replicas,
+                 fraction_A=0.5, omega_kT=0.5, seed=1, init_mode=init, iters_per_pass=iters_per_pass,
+                 device=-1, reserved=0)
+    out = Plan()
+    _check(load().kk_plan_config(ctypes.byref(cfg), int(n_sm), ctypes.byref(out)), "kk_plan_config")
+    d = {name: getattr(out, name) for name, _ in Plan._fields_ if name != "reserved"}
+    d["kernel"] = KERNEL_NAMES[d["kernel"]]
+    return d
 
 
 def launch_count() -> int:

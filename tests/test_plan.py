@@ -1,0 +1,99 @@
+"""Host-side execution planning (kk_plan_config, no GPU needed): which kernel
+kk_sweep launches and the tile shape the cost model picks.  The plan never
+changes results (the GPU parity tests run every kernel against the oracle);
+these checks pin the decisions DESIGN.md documents and the invariants every
+plan must satisfy."""
+import itertools
+import os
+
+import pytest
+
+from paper_1309_4349_b200 import kk
+
+SMEM_2_PER_SM = 113 * 1024     # two 512-thread tile CTAs per SM (228 KB per SM)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    from paper_1309_4349_b200 import build
+    build.build()
+    saved = {k: os.environ.pop(k, None) for k in ("KK_RESIDENT", "KK_BAND", "KK_THI", "KK_TWI", "KK_T",
+                                                  "KK_RES_THREADS")}
+    yield
+    for k, v in saved.items():
+        if v is not None:
+            os.environ[k] = v
+
+
+def test_bench_lattice_plan():
+    p = kk.plan(65536, 65536)
+    assert p["kernel"] == "tile" and p["iters_per_pass"] == 8 and p["halo_rows"] == 24
+    assert p["tile_words"] == 64 and 300 <= p["tile_rows"] <= 340
+    assert p["smem_bytes"] <= SMEM_2_PER_SM          # two CTAs per SM
+    assert p["ctas"] == p["tiles_x"] * p["bands"] >= 148 * 20
+
+
+def test_mid_size_lattice_fills_every_sm():
+    p = kk.plan(4096, 4096)
+    assert p["kernel"] == "tile" and p["ctas"] >= 148
+
+
+def test_small_and_replica_batches_are_resident():
+    assert kk.plan(64, 64)["kernel"] == "resident"
+    assert kk.plan(400, 400)["kernel"] == "resident"             # the paper's lattice
+    p = kk.plan(400, 400, replicas=1024)                           # BASELINE configs[3]
+    assert p["kernel"] == "resident" and p["ctas"] == 1024 and p["threads"] == 256
+    assert kk.plan(400, 400, replicas=100)["threads"] == 512     # all replicas co-resident
+    assert kk.plan(1024, 1024)["kernel"] == "tile"                # one replica too big to stay resident
+    assert kk.plan(1024, 1024, replicas=148)["kernel"] == "resident"
+
+
+def test_slabs_never_use_the_resident_or_band_kernels():
+    p = kk.plan(65536, 8 * 65536, y_begin=65536, y_count=65536)
+    assert p["kernel"] == "tile"
+    q = kk.plan(400, 800, y_begin=400, y_count=400)
+    assert q["kernel"] == "tile"
+
+
+def test_overrides(monkeypatch):
+    monkeypatch.setenv("KK_RESIDENT", "0")
+    assert kk.plan(400, 400)["kernel"] == "tile"
+    monkeypatch.setenv("KK_BAND", "2")
+    assert kk.plan(4096, 4096)["kernel"] == "band"
+    assert kk.plan(4096, 4096)["ctas"] == 148
+    monkeypatch.delenv("KK_BAND")
+    monkeypatch.delenv("KK_RESIDENT")
+    monkeypatch.setenv("KK_THI", "64")
+    monkeypatch.setenv("KK_TWI", "16")
+    p = kk.plan(65536, 65536)
+    assert (p["tile_rows"], p["tile_words"]) == (64, 16)
+    monkeypatch.setenv("KK_THI", "100000")   # cannot fit in shared memory
+    with pytest.raises(kk.KKError):
+        kk.plan(65536, 65536)
+
+
+@pytest.mark.parametrize("Lx,Ly,R,T", list(itertools.product([4, 36, 64, 100, 400, 1000, 4096, 65536],
+                                                               [4, 12, 400, 4096, 65536], [1, 3],
+                                                               [0, 1, 4])))
+def test_plan_invariants(Lx, Ly, R, T):
+    if Lx * Ly * R > 65536 * 65536:
+        pytest.skip("beyond one GPU")
+    p = kk.plan(Lx, Ly, replicas=R, iters_per_pass=T)
+    W = (Lx + 31) // 32
+    assert p["tile_rows"] % 4 == 0 and p["tile_rows"] * p["bands"] >= Ly
+    assert p["tile_rows"] * (p["bands"] - 1) < Ly                 # no empty band
+    assert p["tile_words"] * p["tiles_x"] >= W and p["tile_words"] * (p["tiles_x"] - 1) < W
+    assert 0 < p["smem_bytes"] <= 227 * 1024
+    assert p["halo_rows"] == 3 * (T or 8)
+    if p["kernel"] == "tile":
+        assert p["ctas"] == p["tiles_x"] * p["bands"] * R
+        assert p["smem_bytes"] <= SMEM_2_PER_SM or os.environ.get("KK_THI")
+    elif p["kernel"] == "resident":
+        assert p["ctas"] == R and Lx >= 64 and p["threads"] in (128, 256, 512)
+
+
+def test_invalid_configs_fail_without_a_gpu():
+    for bad in [dict(Lx=10, Ly=8), dict(Lx=8, Ly=6), dict(Lx=8, Ly=8, iters_per_pass=3),
+                dict(Lx=8, Ly=16, y_begin=2, y_count=8)]:
+        with pytest.raises(kk.KKError):
+            kk.plan(**bad)
