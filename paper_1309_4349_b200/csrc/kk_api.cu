@@ -50,7 +50,7 @@ int resident_smem_bytes(const Geom& g);
 int resident_threads(const Geom& g, int64_t replicas, int nsm, int forced);
 cudaError_t launch_resident(const ResParams& P, int64_t replicas, int nt, cudaStream_t stream);
 cudaError_t launch_pass(int T, const PassParams& P, const CUtensorMap& tmap, int grid_y, int replicas,
-                        cudaStream_t stream);
+                        cudaStream_t stream, int threads);
 cudaError_t launch_observe(const ObsParams& P, cudaStream_t s);
 cudaError_t launch_init_block(uint32_t* lat, const Geom& g, int64_t replicas, int64_t nA, cudaStream_t s);
 cudaError_t launch_select_hist(const Geom& g, int64_t rep0, int64_t nrep, int level, const uint32_t* prefix,
@@ -100,6 +100,7 @@ struct kk_lattice {
     int use_tma = 0, box_h = 0;
     int resident = 0;                 // kk_sweep runs the resident kernel (whole replica in shared memory)
     int res_nt = 512;                 // its CTA size
+    int pass_nt = 512;                // tile kernel CTA size (384 or 512)
     int nbands = 0;                   // > 0: kk_sweep runs the band kernel (lattice resident across all SMs)
     uint32_t* xch = nullptr;          // band kernel exchange rows
     unsigned int* band_flags = nullptr;
@@ -304,7 +305,7 @@ int run_pass(kk_lattice* h, int region, const uint32_t* ht, const uint32_t* hb, 
     } else {
         return fail(KK_ERR_ARG, "kk_pass: bad region");
     }
-    KK_CUDA(launch_pass(h->T, P, h->tmap[h->cur], grid_y, (int)h->R, s));  // grid.z = replica (R <= 65535)
+    KK_CUDA(launch_pass(h->T, P, h->tmap[h->cur], grid_y, (int)h->R, s, h->pass_nt));  // grid.z = replica (R <= 65535)
     return KK_OK;
 }
 
@@ -519,6 +520,14 @@ int plan_handle(kk_lattice* h, const kk_config* c, int T, int nsm) {
     // independent handles on separate streams run side by side — 18 x 400^2
     // handles: 33 G/s resident vs 4 G/s for launch-bound tile passes,
     // tools/single_small.py); 2 = whenever the replica fits; 0 = never.
+    // tile kernel CTA size: 384 threads get 80 registers (vs 64 at 512) and
+    // ~4% shorter items (no rematerialised addresses), which wins when there
+    // are many waves of tiles; few-wave grids keep 512 (more warps per tile).
+    {
+        const int forced = env_int("KK_PASS_THREADS", 0);
+        const int64_t ctas = (int64_t)h->tiles_x * h->bands * h->R;
+        h->pass_nt = (forced == 384 || forced == 512) ? forced : (ctas > 4 * (int64_t)nsm ? 384 : 512);
+    }
     const int mode = env_int("KK_RESIDENT", 1);
     const int64_t tile_ctas = (int64_t)h->tiles_x * h->bands;
     const bool small = h->g.Lx * h->g.rows <= 512 * 512;
@@ -574,7 +583,7 @@ int kk_plan_config(const kk_config* c, int n_sm, kk_plan* out) {
     out->bands = tmp.bands;
     out->halo_rows = tmp.hy;
     if (out->kernel == KK_KERNEL_TILE) {
-        out->threads = 512;
+        out->threads = tmp.pass_nt;
         out->smem_bytes = pass_smem_bytes(T, tmp.THI, tmp.TWI);
         out->ctas = (int64_t)tmp.tiles_x * tmp.bands * tmp.R;
     } else if (out->kernel == KK_KERNEL_RESIDENT) {

@@ -43,11 +43,10 @@ namespace kk {
 
 namespace {
 
-#ifndef KK_PASS_THREADS
-#define KK_PASS_THREADS 512
+#ifndef KK_PASS_MIN_BLOCKS
+#define KK_PASS_MIN_BLOCKS 2
 #endif
-constexpr int kThreads = KK_PASS_THREADS;
-constexpr int kMinBlocks = 1024 / kThreads;  // 32 warps per SM at <= 64 registers
+constexpr int kMinBlocks = KK_PASS_MIN_BLOCKS;  // two tile CTAs per SM (shared memory allows two)
 constexpr uint32_t kNib = 0x11111111u;
 
 // Nibble-compressed bit plane of the sites at offset (DX, DY) from the centres
@@ -401,16 +400,16 @@ __device__ __forceinline__ void process_item(const Tabs& S, int r, int w, uint32
     acc.idx_odd += (Sg >> 4) & 0x0F0F0F0Fu;
 }
 
-template <int KX, bool FAST>
+template <int KX, bool FAST, int NT>
 __device__ __forceinline__ void run_iteration(const Tabs& S, int Wt, int r_first, int nrows, uint32_t sweep,
                                               uint32_t c3, const uint32_t* rk, Acc& acc) {
     const int items = nrows * Wt;
     // flattened (row, word) walk without per-item division
     int a = threadIdx.x / Wt;
     int w = threadIdx.x - a * Wt;
-    const int da = kThreads / Wt, dw = kThreads - da * Wt;
+    const int da = NT / Wt, dw = NT - da * Wt;
     int since_flush = 0;
-    for (int it = threadIdx.x; it < items; it += kThreads) {
+    for (int it = threadIdx.x; it < items; it += NT) {
         process_item<KX, 0, FAST>(S, r_first + 4 * a, w, sweep, c3, rk, acc);
         if (++since_flush == 32) {
             acc_flush(acc);
@@ -427,8 +426,8 @@ __device__ __forceinline__ void run_iteration(const Tabs& S, int Wt, int r_first
 
 // FAST: Lx % 32 == 0, so every tile word (halo words included) is an
 // aligned octet of centres and the per-centre draw path is compiled out.
-template <int T, bool FAST>
-__global__ void __launch_bounds__(kThreads, kMinBlocks)
+template <int T, bool FAST, int NT>
+__global__ void __launch_bounds__(NT, kMinBlocks)
     pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassParams P) {
     constexpr int HY = 3 * T;
     const int rep = blockIdx.z;
@@ -455,12 +454,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     uint64_t* tma_bar = reinterpret_cast<uint64_t*>(red + 4 * 16);
     uint2* thr2 = reinterpret_cast<uint2*>(kk_smem + S.th_off);
     uint2* mtab = reinterpret_cast<uint2*>(kk_smem + S.mt_off);
-    for (int b = threadIdx.x; b < 256; b += kThreads)
+    for (int b = threadIdx.x; b < 256; b += NT)
         thr2[b] = make_uint2(P.thr[min(b & 15, 6)], P.thr[min(b >> 4, 6)]);
-    fill_dir_table<kThreads>(S);
+    fill_dir_table<NT>(S);
 
     // ---- per-pass tables
-    for (int w = threadIdx.x; w < Wt; w += kThreads) {
+    for (int w = threadIdx.x; w < Wt; w += NT) {
         const int64_t xu = X0 - 32 + 32 * (int64_t)w;  // unwrapped x of bit 0
         const int64_t xg = wrap_mod(xu, g.Lx);
         mtab[w] = make_uint2((uint32_t)xg, ((xg & 31) == 0 && xg + 32 <= g.Lx) ? 1u : 0u);
@@ -471,7 +470,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
         }
         kk_smem[S.wm_off + w] = own;
     }
-    for (int r = threadIdx.x; r < H; r += kThreads) {
+    for (int r = threadIdx.x; r < H; r += NT) {
         const int64_t y_local = Y0 - HY + r;
         const int64_t yg = wrap_mod(g.y_begin + y_local, g.Ly);
         const bool owned = r >= HY && r < HY + P.THI && y_local < g.rows;
@@ -501,7 +500,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     }
     // no x wrap and whole words: plain contiguous row copies
     const bool contiguous = g.tail == 0 && gw0 >= 0 && gw0 + Wt <= g.W;
-    for (int r = warp; r < (tma_tile ? 0 : H); r += kThreads / 32) {
+    for (int r = warp; r < (tma_tile ? 0 : H); r += NT / 32) {
         const uint32_t* row = row_source(g, src, htop, hbot, HY, Y0 - HY + r);
         const int trow = r * WS + kCol0;
         if (lane < kCol0) {
@@ -569,10 +568,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
         const int r_first = r_lo + ((phase - r_lo) & 3);
         const int nrows = r_hi > r_first ? (r_hi - r_first + 3) / 4 : 0;
         switch (kx) {
-            case 0: run_iteration<0, FAST>(S, Wt, r_first, nrows, P.sweep, c3, P.rk, acc); break;
-            case 1: run_iteration<1, FAST>(S, Wt, r_first, nrows, P.sweep, c3, P.rk, acc); break;
-            case 2: run_iteration<2, FAST>(S, Wt, r_first, nrows, P.sweep, c3, P.rk, acc); break;
-            default: run_iteration<3, FAST>(S, Wt, r_first, nrows, P.sweep, c3, P.rk, acc); break;
+            case 0: run_iteration<0, FAST, NT>(S, Wt, r_first, nrows, P.sweep, c3, P.rk, acc); break;
+            case 1: run_iteration<1, FAST, NT>(S, Wt, r_first, nrows, P.sweep, c3, P.rk, acc); break;
+            case 2: run_iteration<2, FAST, NT>(S, Wt, r_first, nrows, P.sweep, c3, P.rk, acc); break;
+            default: run_iteration<3, FAST, NT>(S, Wt, r_first, nrows, P.sweep, c3, P.rk, acc); break;
         }
         acc_flush(acc);
         __syncthreads();
@@ -586,13 +585,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     if (P.vec_wb && words_out == P.TWI && last_mask == 0xFFFFFFFFu) {
         // 16-byte vectors: P.TWI % 4 == 0, W % 4 == 0, interior column offset 16 B
         const int vpr = P.TWI / 4;  // vectors per row
-        for (int i = threadIdx.x; i < rows_out * vpr; i += kThreads) {
+        for (int i = threadIdx.x; i < rows_out * vpr; i += NT) {
             const int r = i / vpr, v = i - r * vpr;
             const uint4 val = *reinterpret_cast<const uint4*>(kk_smem + (HY + r) * WS + kCol0 + 1 + 4 * v);
             *reinterpret_cast<uint4*>(dst + (int64_t)r * g.W + 4 * v) = val;
         }
     } else {
-        for (int r = warp; r < rows_out; r += kThreads / 32) {
+        for (int r = warp; r < rows_out; r += NT / 32) {
             uint32_t* drow = dst + (int64_t)r * g.W;
             const int trow = (HY + r) * WS + kCol0 + 1;  // tile word 1 = first interior word
             for (int w = lane; w < words_out; w += 32)
@@ -612,15 +611,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
         v3 += __shfl_xor_sync(0xFFFFFFFFu, v3, o);
     }
     if (lane == 0) {
-        red[0 * (kThreads / 32) + warp] = v0;
-        red[1 * (kThreads / 32) + warp] = v1;
-        red[2 * (kThreads / 32) + warp] = v2;
-        red[3 * (kThreads / 32) + warp] = (unsigned long long)v3;
+        red[0 * (NT / 32) + warp] = v0;
+        red[1 * (NT / 32) + warp] = v1;
+        red[2 * (NT / 32) + warp] = v2;
+        red[3 * (NT / 32) + warp] = (unsigned long long)v3;
     }
     __syncthreads();
     if (threadIdx.x < 4) {
         unsigned long long s = 0;
-        for (int k = 0; k < kThreads / 32; ++k) s += red[threadIdx.x * (kThreads / 32) + k];
+        for (int k = 0; k < NT / 32; ++k) s += red[threadIdx.x * (NT / 32) + k];
         if (s) atomicAdd(P.stats + rep * 4 + threadIdx.x, s);
     }
 }
@@ -1170,22 +1169,28 @@ cudaError_t launch_band(const BandParams& P, cudaStream_t stream) {
 }
 
 cudaError_t launch_pass(int T, const PassParams& P, const CUtensorMap& tmap, int grid_y, int replicas,
-                        cudaStream_t stream) {
+                        cudaStream_t stream, int threads) {
     const int smem = pass_smem_bytes(T, P.THI, P.TWI);
     dim3 grid(P.tiles_x, grid_y, replicas);
     if (grid_y == 0) return cudaSuccess;
     cudaError_t e = cudaSuccess;
-#define KK_LAUNCH(TT)                                                                                  \
-    case TT:                                                                                           \
-        if (P.g.tail == 0) {                                                                           \
-            e = ensure_dynamic_smem((const void*)pass_kernel<TT, true>, smem); \
-            if (e != cudaSuccess) return e;                                                            \
-            pass_kernel<TT, true><<<grid, kThreads, smem, stream>>>(tmap, P);                          \
-        } else {                                                                                       \
-            e = ensure_dynamic_smem((const void*)pass_kernel<TT, false>, smem); \
-            if (e != cudaSuccess) return e;                                                            \
-            pass_kernel<TT, false><<<grid, kThreads, smem, stream>>>(tmap, P);                         \
-        }                                                                                              \
+#define KK_LAUNCH_NT(TT, NTT)                                                                   \
+    if (P.g.tail == 0) {                                                                        \
+        e = ensure_dynamic_smem((const void*)pass_kernel<TT, true, NTT>, smem);                 \
+        if (e != cudaSuccess) return e;                                                         \
+        pass_kernel<TT, true, NTT><<<grid, NTT, smem, stream>>>(tmap, P);                       \
+    } else {                                                                                    \
+        e = ensure_dynamic_smem((const void*)pass_kernel<TT, false, NTT>, smem);                \
+        if (e != cudaSuccess) return e;                                                         \
+        pass_kernel<TT, false, NTT><<<grid, NTT, smem, stream>>>(tmap, P);                      \
+    }
+#define KK_LAUNCH(TT)                                                                           \
+    case TT:                                                                                    \
+        if (threads == 384) {                                                                   \
+            KK_LAUNCH_NT(TT, 384)                                                               \
+        } else {                                                                                \
+            KK_LAUNCH_NT(TT, 512)                                                               \
+        }                                                                                       \
         break;
     switch (T) {
         KK_LAUNCH(1)
@@ -1195,6 +1200,7 @@ cudaError_t launch_pass(int T, const PassParams& P, const CUtensorMap& tmap, int
         default:
             return cudaErrorInvalidValue;
     }
+#undef KK_LAUNCH_NT
 #undef KK_LAUNCH
     count_launch();
     return cudaGetLastError();

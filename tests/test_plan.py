@@ -18,7 +18,7 @@ def _lib():
     from paper_1309_4349_b200 import build
     build.build()
     saved = {k: os.environ.pop(k, None) for k in ("KK_RESIDENT", "KK_BAND", "KK_THI", "KK_TWI", "KK_T",
-                                                  "KK_RES_THREADS")}
+                                                  "KK_RES_THREADS", "KK_PASS_THREADS")}
     yield
     for k, v in saved.items():
         if v is not None:
@@ -31,11 +31,12 @@ def test_bench_lattice_plan():
     assert p["tile_words"] == 64 and 300 <= p["tile_rows"] <= 340
     assert p["smem_bytes"] <= SMEM_2_PER_SM          # two CTAs per SM
     assert p["ctas"] == p["tiles_x"] * p["bands"] >= 148 * 20
+    assert p["threads"] == 384                      # many waves: 80-register CTAs
 
 
 def test_mid_size_lattice_fills_every_sm():
     p = kk.plan(4096, 4096)
-    assert p["kernel"] == "tile" and p["ctas"] >= 148
+    assert p["kernel"] == "tile" and p["ctas"] >= 148 and p["threads"] == 512
 
 
 def test_small_and_replica_batches_are_resident():
