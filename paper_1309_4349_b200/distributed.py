@@ -292,6 +292,14 @@ class Simulation:
     def upload_packed(self, host_ptr: int):
         self.lat.set_packed_ptr(host_ptr, self.driver.stream)
 
+    def upload_device(self, dev_ptr: int, stream=None):
+        """Lattice <- packed words at a device address (same layout)."""
+        self.lat.copy_packed_device(dev_ptr, True, stream if stream is not None else self.driver.stream)
+
+    def download_device(self, dev_ptr: int, stream=None):
+        """Packed words of the lattice -> a device address."""
+        self.lat.copy_packed_device(dev_ptr, False, stream if stream is not None else self.driver.stream)
+
     def download_packed(self, host_ptr: int):
         import ctypes
         kk._check(kk.load().kk_get_lattice_packed(self.lat.handle, ctypes.c_void_p(host_ptr),
