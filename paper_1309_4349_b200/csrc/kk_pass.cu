@@ -451,7 +451,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks)
     S.th_off = P.th_off;
     S.dt_off = P.dt_off;
     unsigned long long* red = reinterpret_cast<unsigned long long*>(kk_smem + P.red_off);  // [4][warps]
-    uint64_t* tma_bar = reinterpret_cast<uint64_t*>(red + 4 * 16);
+    uint64_t* tma_bar = reinterpret_cast<uint64_t*>(red + 4 * 32);
     uint2* thr2 = reinterpret_cast<uint2*>(kk_smem + S.th_off);
     uint2* mtab = reinterpret_cast<uint2*>(kk_smem + S.mt_off);
     for (int b = threadIdx.x; b < 256; b += NT)

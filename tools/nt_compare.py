@@ -1,5 +1,5 @@
-"""Tile-kernel CTA size 384 vs 512 (KK_PASS_THREADS) across lattice sizes.
-Usage: python tools/nt_compare.py"""
+"""Tile-kernel CTA size (KK_PASS_THREADS) across lattice sizes.
+Usage: python tools/nt_compare.py [sizes...]"""
 import os
 import sys
 
@@ -10,7 +10,8 @@ from paper_1309_4349_b200 import kk  # noqa: E402
 
 torch.cuda.set_device(0)
 s = torch.cuda.current_stream()
-for L_ in (2048, 4096, 8192, 16384, 32768, 65536):
+sizes = [int(a) for a in sys.argv[1:]] or [2048, 4096, 8192, 16384, 32768, 65536]
+for L_ in sizes:
     line = f"{L_}^2:"
     for nt in (384, 512):
         os.environ["KK_PASS_THREADS"] = str(nt)
