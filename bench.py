@@ -194,11 +194,18 @@ def main():
         return
     import torch
     assert torch.cuda.is_available(), "bench.py needs a CUDA device"
+    # KK_BENCH_BACKEND=gloo + KK_BENCH_DEVICE=0: functional runs of the N>1
+    # path with several ranks on one GPU (NCCL refuses that); never for numbers
+    backend = os.environ.get("KK_BENCH_BACKEND", "nccl")
+    local = int(os.environ.get("KK_BENCH_DEVICE", local))
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_1309_4349_b200 import build as B
     if rank == 0:
         B.build()
@@ -253,7 +260,7 @@ def main():
     ms = t0.elapsed_time(t1)
     pass_ms = [e0.elapsed_time(e1) for e0, e1 in pass_events]
     if dist:
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor([ms], device="cuda" if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_per_step = ms / a.steps
@@ -344,7 +351,7 @@ def main():
         wall = time.perf_counter() - w0
         e_ms = max(s0.elapsed_time(s1), wall * 1e3)
         if dist:
-            t = torch.tensor([e_ms], device="cuda")
+            t = torch.tensor([e_ms], device="cuda" if backend == "nccl" else "cpu")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
         nbytes = words * 4
@@ -364,7 +371,10 @@ def main():
                                    + ("" if a.no_ccl else " + cluster histogram") + " per step",
                        "omega_kT": a.omega, "fraction_A": a.fraction, "start": "random",
                        "iters_per_pass": a.T, "parallelism": f"slab{world}",
-                       "l2": "inputs larger than L2 (2 x 512 MiB bit-packed per GPU)"},
+                       "l2": (f"inputs larger than L2 (2 x {Lx * rows // 8 // 2**20} MiB bit-packed per GPU)"
+                              if Lx * rows // 8 > 126 * 2**20 else
+                              f"lattice ({Lx * rows // 8 // 2**20} MiB per buffer) fits in L2: small-case run, "
+                              "not a bench configuration")},
             "roofline": roof,
             "gpu_launches": launches,
             "clocks": clk.summary(),

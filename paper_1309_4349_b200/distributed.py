@@ -31,7 +31,11 @@ from . import kk
 
 # ----------------------------------------------------------------------- comm
 class TorchComm:
-    """torch.distributed plumbing: sums, gathers and the halo exchange."""
+    """torch.distributed plumbing: sums, gathers and the halo exchange.
+
+    With NCCL (the product configuration) device tensors move directly.  With
+    gloo and CUDA tensors (functional multi-rank tests on a single GPU, where
+    NCCL refuses two ranks per device) they are staged through host memory."""
 
     TAG_DOWN, TAG_UP = 11, 12
 
@@ -41,11 +45,15 @@ class TorchComm:
         self.torch, self.dist = torch, dist
         self.rank, self.world, self.group = rank, world, group
         self.device = device if device is not None else torch.device("cpu")
+        self.stage = False
+        if world > 1 and self.device.type == "cuda":
+            self.stage = dist.get_backend(group) == "gloo"
+        self.coll_device = torch.device("cpu") if self.stage else self.device
 
     def all_reduce_sum(self, a: np.ndarray) -> np.ndarray:
         if self.world == 1:
             return a
-        t = self.torch.from_numpy(np.ascontiguousarray(a, np.int64)).to(self.device)
+        t = self.torch.from_numpy(np.ascontiguousarray(a, np.int64)).to(self.coll_device)
         self.dist.all_reduce(t, group=self.group)
         return t.cpu().numpy()
 
@@ -54,14 +62,14 @@ class TorchComm:
         if self.world == 1:
             return a
         torch = self.torch
-        n = torch.tensor([a.shape[0]], dtype=torch.int64, device=self.device)
+        n = torch.tensor([a.shape[0]], dtype=torch.int64, device=self.coll_device)
         ns = [torch.zeros_like(n) for _ in range(self.world)]
         self.dist.all_gather(ns, n, group=self.group)
         m = max(int(x.item()) for x in ns)
         k = a.shape[1]
         pad = np.zeros((max(m, 1), k), np.int64)
         pad[: a.shape[0]] = a
-        t = torch.from_numpy(pad).to(self.device)
+        t = torch.from_numpy(pad).to(self.coll_device)
         outs = [torch.zeros_like(t) for _ in range(self.world)]
         self.dist.all_gather(outs, t, group=self.group)
         return np.concatenate([o.cpu().numpy()[: int(c.item())] for o, c in zip(outs, ns)], axis=0)
@@ -69,15 +77,24 @@ class TorchComm:
     def all_gather_tensor(self, t):
         if self.world == 1:
             return [t]
-        outs = [self.torch.empty_like(t) for _ in range(self.world)]
-        self.dist.all_gather(outs, t, group=self.group)
-        return outs
+        src = t.cpu() if self.stage else t
+        outs = [self.torch.empty_like(src) for _ in range(self.world)]
+        self.dist.all_gather(outs, src, group=self.group)
+        return [o.to(t.device) for o in outs] if self.stage else outs
 
     def exchange_start(self, send_top, send_bot, recv_top, recv_bot):
         """send_top -> rank-1 (its bottom halo); send_bot -> rank+1 (its top halo)."""
         dist = self.dist
         prev = (self.rank - 1) % self.world
         nxt = (self.rank + 1) % self.world
+        if self.stage:
+            st, sb = send_top.cpu(), send_bot.cpu()
+            rt, rb = self.torch.empty_like(st), self.torch.empty_like(sb)
+            ops = [dist.P2POp(dist.isend, st, prev, self.group, self.TAG_DOWN),
+                   dist.P2POp(dist.irecv, rb, nxt, self.group, self.TAG_DOWN),
+                   dist.P2POp(dist.isend, sb, nxt, self.group, self.TAG_UP),
+                   dist.P2POp(dist.irecv, rt, prev, self.group, self.TAG_UP)]
+            return [_StagedRecv(dist.batch_isend_irecv(ops), [(rt, recv_top), (rb, recv_bot)])]
         ops = [dist.P2POp(dist.isend, send_top, prev, self.group, self.TAG_DOWN),
                dist.P2POp(dist.irecv, recv_bot, nxt, self.group, self.TAG_DOWN),
                dist.P2POp(dist.isend, send_bot, nxt, self.group, self.TAG_UP),
@@ -88,6 +105,19 @@ class TorchComm:
     def exchange_wait(works):
         for w in works:
             w.wait()
+
+
+class _StagedRecv:
+    """Host-staged exchange: wait for the host receives, then copy to device."""
+
+    def __init__(self, works, copies):
+        self.works, self.copies = works, copies
+
+    def wait(self):
+        for w in self.works:
+            w.wait()
+        for host, dev in self.copies:
+            dev.copy_(host)
 
 
 # -------------------------------------------------------------- GPU backend
