@@ -408,6 +408,20 @@ __device__ __forceinline__ void run_iteration(const Tabs& S, int Wt, int r_first
     int a = threadIdx.x / Wt;
     int w = threadIdx.x - a * Wt;
     const int da = NT / Wt, dw = NT - da * Wt;
+    if (items <= 40 * NT) {
+        // at most 40 items per thread: the byte-lane sums (<= 6 per item)
+        // cannot overflow before the caller's flush after the iteration
+        for (int it = threadIdx.x; it < items; it += NT) {
+            process_item<KX, 0, FAST>(S, r_first + 4 * a, w, sweep, c3, rk, acc);
+            a += da;
+            w += dw;
+            if (w >= Wt) {
+                w -= Wt;
+                ++a;
+            }
+        }
+        return;
+    }
     int since_flush = 0;
     for (int it = threadIdx.x; it < items; it += NT) {
         process_item<KX, 0, FAST>(S, r_first + 4 * a, w, sweep, c3, rk, acc);
@@ -685,6 +699,18 @@ __device__ __forceinline__ void res_iteration(const Tabs& S, int r_first, uint32
     int a = threadIdx.x / W;
     int w = threadIdx.x - a * W;
     const int da = NT / W, dw = NT - da * W;
+    if (items <= 40 * NT) {  // no byte-lane overflow before the flush after the iteration
+        for (int it = threadIdx.x; it < items; it += NT) {
+            process_item<KX, 1, true>(S, r_first + 4 * a, w + 1, sweep, c3, rk, acc);
+            a += da;
+            w += dw;
+            if (w >= W) {
+                w -= W;
+                ++a;
+            }
+        }
+        return;
+    }
     int since_flush = 0;
     for (int it = threadIdx.x; it < items; it += NT) {
         process_item<KX, 1, true>(S, r_first + 4 * a, w + 1, sweep, c3, rk, acc);
