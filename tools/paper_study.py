@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--every", type=int, default=1000)
     ap.add_argument("--L", type=int, default=400)
     ap.add_argument("--seed", type=int, default=1309)
+    ap.add_argument("--seeds", type=int, default=1, help="independent replicas per (f, omega) point")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     torch.cuda.set_device(0)
@@ -38,7 +39,7 @@ def main():
     fracs = [0.5, 0.3]
     pts = [(f, om) for f in fracs for om in omegas]
     streams = [torch.cuda.Stream() for _ in pts]
-    lats = [kk.Lattice(a.L, a.L, f, om, a.seed + i) for i, (f, om) in enumerate(pts)]
+    lats = [kk.Lattice(a.L, a.L, f, om, a.seed + i, replicas=a.seeds) for i, (f, om) in enumerate(pts)]
     N = a.L * a.L
     acc = [{"nab": [], "mean_size": [], "largest": [], "n_clusters": []} for _ in pts]
     t0 = time.perf_counter()
@@ -51,27 +52,27 @@ def main():
         if done <= a.sweeps // 2:
             continue
         for i, (L, s) in enumerate(zip(lats, streams)):
-            nab = int(L.energy(stream=s)[0][0])
-            h = L.cluster_histogram(1, stream=s)[0]
-            sizes = np.array([sz for sz, _ in h], np.float64)
-            counts = np.array([c for _, c in h], np.float64)
-            acc[i]["nab"].append(nab / N)
-            acc[i]["n_clusters"].append(counts.sum())
-            acc[i]["mean_size"].append(float((sizes * counts).sum() / counts.sum()))
-            acc[i]["largest"].append(float(sizes.max() / N))
+            nab = L.energy(stream=s)[0]
+            for r, h in enumerate(L.cluster_histogram(1, stream=s)):
+                sizes = np.array([sz for sz, _ in h], np.float64)
+                counts = np.array([c for _, c in h], np.float64)
+                acc[i]["nab"].append(int(nab[r]) / N)
+                acc[i]["n_clusters"].append(counts.sum())
+                acc[i]["mean_size"].append(float((sizes * counts).sum() / counts.sum()))
+                acc[i]["largest"].append(float(sizes.max() / N))
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     rows = []
     for (f, om), L, d in zip(pts, lats, acc):
-        st = L.stats()[0]
-        row = {"fraction_A": f, "omega_kT": om, "sweeps": a.sweeps, "samples": len(d["nab"]),
+        st = L.stats().sum(axis=0)
+        row = {"fraction_A": f, "omega_kT": om, "sweeps": a.sweeps, "replicas": a.seeds, "samples": len(d["nab"]),
                "nab_per_site": float(np.mean(d["nab"])), "mean_cluster_size_A": float(np.mean(d["mean_size"])),
                "clusters_A": float(np.mean(d["n_clusters"])), "largest_A_fraction": float(np.mean(d["largest"])),
                "acceptance": float(st[2] / max(st[0], 1))}
         rows.append(row)
         print(json.dumps(row), flush=True)
-    total = a.sweeps * N * len(pts)
-    print(f"# {len(pts)} lattices of {a.L}x{a.L}, {a.sweeps} sweeps each: {wall:.1f} s wall, "
+    total = a.sweeps * N * len(pts) * a.seeds
+    print(f"# {len(pts)} x {a.seeds} lattices of {a.L}x{a.L}, {a.sweeps} sweeps each: {wall:.1f} s wall, "
           f"{total / wall / 1e9:.1f} G site-updates/s aggregate (incl. sampling)", flush=True)
     print("# f     omega  N_AB/site  <cluster size>  largest/N  acceptance")
     for r in rows:
