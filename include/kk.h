@@ -116,7 +116,8 @@ int kk_destroy(kk_handle h);
  * larger lattices the tile kernel (16/T launches per sweep);
  * environment overrides for testing: KK_RESIDENT=0/2 (never/always when it
  * fits), KK_BAND=2 (band kernel), KK_THI/KK_TWI (tile shape),
- * KK_RES_THREADS=128/256/512. */
+ * KK_RES_THREADS=128/256/512, KK_PASS_THREADS=384/512, KK_TMA=0 (LDG
+ * instead of TMA staging). */
 int kk_sweep(kk_handle h, int64_t n, void* stream);
 
 /* Energy per replica (R3): nab_out[r] = N_AB (unlike nearest-neighbour pairs,

@@ -264,11 +264,9 @@ PassParams make_pass_params(kk_lattice* h, const uint32_t* ht, const uint32_t* h
 void make_tensor_maps(kk_lattice* h) {
     h->use_tma = 0;
     const int WS = h->TWI + 8, H = h->THI + 6 * h->T;
-    // Opt-in (KK_TMA=1): on the round-1 B200 image the in-kernel TMA staging
-    // raised "illegal instruction" although the same descriptor and PTX work in
-    // tools/tma_probe.cu; root cause open, so the default staging is
-    // the coalesced LDG path.
-    if (h->g.tail != 0 || h->g.W % 4 != 0 || WS % 4 != 0 || WS > 256 || !env_int("KK_TMA", 0)) return;
+    // TMA staging of interior tiles (default; KK_TMA=0 selects the LDG path):
+    // +6% on the 65536^2 bench lattice (tools/tma_rate.py).
+    if (h->g.tail != 0 || h->g.W % 4 != 0 || WS % 4 != 0 || WS > 256 || !env_int("KK_TMA", 1)) return;
     PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode), cudaEnableDefault,

@@ -468,6 +468,25 @@ __global__ void __launch_bounds__(NT, kMinBlocks)
     uint64_t* tma_bar = reinterpret_cast<uint64_t*>(red + 4 * 32);
     uint2* thr2 = reinterpret_cast<uint2*>(kk_smem + S.th_off);
     uint2* mtab = reinterpret_cast<uint2*>(kk_smem + S.mt_off);
+
+    // ---- stage tile + halo, part 1: TMA.  A tile whose rows and words (guard
+    // columns included) all lie inside this handle's lattice is copied by a
+    // few 3D boxes (WS words x box_h rows x 1 replica) starting at word
+    // gw0 - kCol0 (smem column 0); the copy is issued first and runs while the
+    // threads build the per-pass tables.
+    const int64_t gw0 = X0 / 32 - 1;
+    const bool tma_tile = P.use_tma && Y0 - HY >= 0 && Y0 - HY + H <= g.rows && gw0 - kCol0 >= 0 &&
+                          gw0 - kCol0 + WS <= g.W;
+    if (tma_tile && threadIdx.x == 0) {
+        mbar_init(tma_bar, 1);
+        const int nbox = (H + P.box_h - 1) / P.box_h;
+        mbar_expect_tx(tma_bar, (uint32_t)(nbox * P.box_h * WS * 4));
+        for (int b = 0; b < nbox; ++b) {
+            const int y0 = min(b * P.box_h, H - P.box_h);  // last box may overlap the previous one
+            tma_load_3d(smem_u32(kk_smem + y0 * WS), &tmap, tma_bar, (int)(gw0 - kCol0), (int)(Y0 - HY + y0),
+                        rep);
+        }
+    }
     for (int b = threadIdx.x; b < 256; b += NT)
         thr2[b] = make_uint2(P.thr[min(b & 15, 6)], P.thr[min(b >> 4, 6)]);
     fill_dir_table<NT>(S);
@@ -491,25 +510,11 @@ __global__ void __launch_bounds__(NT, kMinBlocks)
         kk_smem[S.rl_off + r] = (uint32_t)(yg >> 2) | (owned ? 0x80000000u : 0u);
     }
 
-    // ---- stage tile + halo
+    // ---- stage tile + halo, part 2: wait for the TMA boxes (the barrier
+    // makes thread 0's mbarrier init visible first), or copy with LDG
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t gw0 = X0 / 32 - 1;
-    // TMA: a tile whose rows and words all lie inside this handle's lattice is
-    // copied by a few 3D boxes (WS words x box_h rows x 1 replica) starting at
-    // word gw0 - (kCol0 - 1); guard columns receive real (or zero OOB) data.
-    const bool tma_tile = P.use_tma && Y0 - HY >= 0 && Y0 - HY + H <= g.rows && gw0 >= 0 && gw0 + Wt <= g.W;
     if (tma_tile) {
-        if (threadIdx.x == 0) mbar_init(tma_bar, 1);
         __syncthreads();
-        if (threadIdx.x == 0) {
-            const int nbox = (H + P.box_h - 1) / P.box_h;
-            mbar_expect_tx(tma_bar, (uint32_t)(nbox * P.box_h * WS * 4));
-            for (int b = 0; b < nbox; ++b) {
-                const int y0 = min(b * P.box_h, H - P.box_h);  // last box may overlap the previous one
-                tma_load_3d(smem_u32(kk_smem + y0 * WS), &tmap, tma_bar, (int)(gw0 - (kCol0 - 1)),
-                            (int)(Y0 - HY + y0), rep);
-            }
-        }
         mbar_wait(tma_bar, 0);
     }
     // no x wrap and whole words: plain contiguous row copies
