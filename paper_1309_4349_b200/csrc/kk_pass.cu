@@ -440,9 +440,26 @@ __device__ __forceinline__ void run_iteration(const Tabs& S, int Wt, int r_first
 
 // FAST: Lx % 32 == 0, so every tile word (halo words included) is an
 // aligned octet of centres and the per-centre draw path is compiled out.
+// Phase clocks of one CTA (tile (1,1) of replica 0), compiled only with
+// -DKK_PASS_CLK for tools/pass_clocks.py: staging+setup, items, iteration
+// barriers, write-back.
+#ifdef KK_PASS_CLK
+__device__ unsigned long long kk_pass_clk[16];
+#define KK_PCLK(k)                                                                  \
+    if (threadIdx.x == 0 && blockIdx.x == 1 && blockIdx.y == 1 && blockIdx.z == 0) { \
+        const long long c1 = clock64();                                             \
+        atomicAdd(&kk_pass_clk[k], (unsigned long long)(c1 - c0clk));              \
+        c0clk = c1;                                                                 \
+    }
+#else
+#define KK_PCLK(k)
+#endif
 template <int T, bool FAST, int NT>
 __global__ void __launch_bounds__(NT, kMinBlocks)
     pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassParams P) {
+#ifdef KK_PASS_CLK
+    long long c0clk = clock64();
+#endif
     constexpr int HY = 3 * T;
     const int rep = blockIdx.z;
     const int band = (int)blockIdx.y < P.nA ? P.bA + (int)blockIdx.y : P.bB + ((int)blockIdx.y - P.nA);
@@ -550,6 +567,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks)
         }
     }
     __syncthreads();
+    KK_PCLK(0)
 
     const Words4 sched = philox10(0u, 0u, P.sweep, ((uint32_t)rep << 8) | kTagSchedule, P.key0, P.key1);
     Acc acc = {0u, 0u, 0u, 0u, 0u, 0ull};
@@ -593,7 +611,9 @@ __global__ void __launch_bounds__(NT, kMinBlocks)
             default: run_iteration<3, FAST, NT>(S, Wt, r_first, nrows, P.sweep, c3, P.rk, acc); break;
         }
         acc_flush(acc);
+        KK_PCLK(1)
         __syncthreads();
+        KK_PCLK(2)
     }
 
     // ---- write the interior to the other buffer
@@ -618,6 +638,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks)
         }
     }
 
+    KK_PCLK(3)
     // ---- counters: warp reduce, block reduce, one atomic per CTA per counter
     unsigned long long v0 = acc.attempted, v1 = acc.trivial, v2 = acc.accepted;
     // sum over accepted owned centres of dN_AB = 2 v = 2 (idx - 3)
@@ -1198,6 +1219,15 @@ cudaError_t launch_band(const BandParams& P, cudaStream_t stream) {
     count_launch();
     return cudaGetLastError();
 }
+
+#ifdef KK_PASS_CLK
+extern "C" int kk_debug_pass_clocks(unsigned long long* out) {
+    cudaMemcpyFromSymbol(out, kk_pass_clk, sizeof(kk_pass_clk));
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(kk_pass_clk, z, sizeof(z));
+    return 0;
+}
+#endif
 
 cudaError_t launch_pass(int T, const PassParams& P, const CUtensorMap& tmap, int grid_y, int replicas,
                         cudaStream_t stream, int threads) {
