@@ -159,6 +159,20 @@ int env_int(const char* name, int dflt) {
     return (v && *v) ? std::atoi(v) : dflt;
 }
 
+// Temporary device buffer freed on every return path (the KK_CUDA early
+// returns included).
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    cudaError_t alloc(size_t n) { return cudaMalloc(&p, sizeof(T) * (n ? n : 1)); }
+};
+
 int64_t count_a_for(int64_t N, double f) { return (int64_t)std::floor(f * (double)N + 0.5); }
 
 // R5: accept iff u32 <= thr[v+3], thr = ceil(exp(-dE) 2^32) - 1, dE = omega*2v.
@@ -339,19 +353,17 @@ int select_hist(kk_lattice* h, int level, const uint32_t* prefix, int64_t* hist_
     const uint32_t k0 = (uint32_t)(h->seed & 0xFFFFFFFFu), k1 = (uint32_t)(h->seed >> 32);
     for (int64_t r0 = 0; r0 < h->R; r0 += 65535) {
         const int64_t nr = std::min<int64_t>(65535, h->R - r0);
-        unsigned long long* dhist = nullptr;
-        uint32_t* dpre = nullptr;
-        KK_CUDA(cudaMalloc(&dhist, sizeof(unsigned long long) * nr * 2048));
-        KK_CUDA(cudaMalloc(&dpre, sizeof(uint32_t) * nr));
-        KK_CUDA(cudaMemsetAsync(dhist, 0, sizeof(unsigned long long) * nr * 2048, s));
-        if (prefix) KK_CUDA(cudaMemcpyAsync(dpre, prefix + r0, sizeof(uint32_t) * nr, cudaMemcpyHostToDevice, s));
-        else KK_CUDA(cudaMemsetAsync(dpre, 0, sizeof(uint32_t) * nr, s));
-        KK_CUDA(launch_select_hist(h->g, r0, nr, level, dpre, dhist, k0, k1, s));
-        KK_CUDA(cudaMemcpyAsync(hist_out + r0 * 2048, dhist, sizeof(unsigned long long) * nr * 2048,
+        DevBuf<unsigned long long> dhist;
+        DevBuf<uint32_t> dpre;
+        KK_CUDA(dhist.alloc((size_t)nr * 2048));
+        KK_CUDA(dpre.alloc((size_t)nr));
+        KK_CUDA(cudaMemsetAsync(dhist.p, 0, sizeof(unsigned long long) * nr * 2048, s));
+        if (prefix) KK_CUDA(cudaMemcpyAsync(dpre.p, prefix + r0, sizeof(uint32_t) * nr, cudaMemcpyHostToDevice, s));
+        else KK_CUDA(cudaMemsetAsync(dpre.p, 0, sizeof(uint32_t) * nr, s));
+        KK_CUDA(launch_select_hist(h->g, r0, nr, level, dpre.p, dhist.p, k0, k1, s));
+        KK_CUDA(cudaMemcpyAsync(hist_out + r0 * 2048, dhist.p, sizeof(unsigned long long) * nr * 2048,
                                 cudaMemcpyDeviceToHost, s));
         KK_CUDA(cudaStreamSynchronize(s));
-        cudaFree(dhist);
-        cudaFree(dpre);
     }
     return KK_OK;
 }
@@ -362,22 +374,22 @@ int select_ties(kk_lattice* h, const uint32_t* K, int64_t* out, int64_t capacity
     for (int64_t r0 = 0; r0 < h->R; r0 += 65535) {
         const int64_t nr = std::min<int64_t>(65535, h->R - r0);
         const int64_t cap = std::max<int64_t>(0, capacity - total);
-        uint32_t* dK = nullptr;
-        long long* dties = nullptr;
-        unsigned long long* dcount = nullptr;
-        KK_CUDA(cudaMalloc(&dK, sizeof(uint32_t) * nr));
-        KK_CUDA(cudaMalloc(&dties, sizeof(long long) * 2 * std::max<int64_t>(cap, 1)));
-        KK_CUDA(cudaMalloc(&dcount, sizeof(unsigned long long)));
-        KK_CUDA(cudaMemsetAsync(dcount, 0, sizeof(unsigned long long), s));
-        KK_CUDA(cudaMemcpyAsync(dK, K + r0, sizeof(uint32_t) * nr, cudaMemcpyHostToDevice, s));
-        KK_CUDA(launch_select_ties(h->g, r0, nr, dK, dties, dcount, cap, k0, k1, s));
+        DevBuf<uint32_t> dK;
+        DevBuf<long long> dties;
+        DevBuf<unsigned long long> dcount;
+        KK_CUDA(dK.alloc((size_t)nr));
+        KK_CUDA(dties.alloc(2 * (size_t)std::max<int64_t>(cap, 1)));
+        KK_CUDA(dcount.alloc(1));
+        KK_CUDA(cudaMemsetAsync(dcount.p, 0, sizeof(unsigned long long), s));
+        KK_CUDA(cudaMemcpyAsync(dK.p, K + r0, sizeof(uint32_t) * nr, cudaMemcpyHostToDevice, s));
+        KK_CUDA(launch_select_ties(h->g, r0, nr, dK.p, dties.p, dcount.p, cap, k0, k1, s));
         unsigned long long nt = 0;
-        KK_CUDA(cudaMemcpyAsync(&nt, dcount, sizeof(nt), cudaMemcpyDeviceToHost, s));
+        KK_CUDA(cudaMemcpyAsync(&nt, dcount.p, sizeof(nt), cudaMemcpyDeviceToHost, s));
         KK_CUDA(cudaStreamSynchronize(s));
         const int64_t got = std::min<int64_t>((int64_t)nt, cap);
         if (got > 0 && out) {
             std::vector<long long> tmp(2 * got);
-            KK_CUDA(cudaMemcpyAsync(tmp.data(), dties, sizeof(long long) * 2 * got, cudaMemcpyDeviceToHost, s));
+            KK_CUDA(cudaMemcpyAsync(tmp.data(), dties.p, sizeof(long long) * 2 * got, cudaMemcpyDeviceToHost, s));
             KK_CUDA(cudaStreamSynchronize(s));
             for (int64_t t = 0; t < got; ++t) {
                 out[2 * (total + t)] = tmp[2 * t] + r0;
@@ -385,9 +397,6 @@ int select_ties(kk_lattice* h, const uint32_t* K, int64_t* out, int64_t capacity
             }
         }
         total += (int64_t)nt;
-        cudaFree(dK);
-        cudaFree(dties);
-        cudaFree(dcount);
     }
     *n_out = total;
     if (total > capacity) return fail(KK_ERR_CAPACITY, "tie buffer too small");
@@ -398,16 +407,14 @@ int select_apply(kk_lattice* h, const uint32_t* K, const int64_t* cut, cudaStrea
     const uint32_t k0 = (uint32_t)(h->seed & 0xFFFFFFFFu), k1 = (uint32_t)(h->seed >> 32);
     for (int64_t r0 = 0; r0 < h->R; r0 += 65535) {
         const int64_t nr = std::min<int64_t>(65535, h->R - r0);
-        uint32_t* dK = nullptr;
-        long long* dcut = nullptr;
-        KK_CUDA(cudaMalloc(&dK, sizeof(uint32_t) * nr));
-        KK_CUDA(cudaMalloc(&dcut, sizeof(long long) * nr));
-        KK_CUDA(cudaMemcpyAsync(dK, K + r0, sizeof(uint32_t) * nr, cudaMemcpyHostToDevice, s));
-        KK_CUDA(cudaMemcpyAsync(dcut, cut + r0, sizeof(long long) * nr, cudaMemcpyHostToDevice, s));
-        KK_CUDA(launch_select_apply(h->buf[h->cur], h->g, r0, nr, dK, dcut, k0, k1, s));
+        DevBuf<uint32_t> dK;
+        DevBuf<long long> dcut;
+        KK_CUDA(dK.alloc((size_t)nr));
+        KK_CUDA(dcut.alloc((size_t)nr));
+        KK_CUDA(cudaMemcpyAsync(dK.p, K + r0, sizeof(uint32_t) * nr, cudaMemcpyHostToDevice, s));
+        KK_CUDA(cudaMemcpyAsync(dcut.p, cut + r0, sizeof(long long) * nr, cudaMemcpyHostToDevice, s));
+        KK_CUDA(launch_select_apply(h->buf[h->cur], h->g, r0, nr, dK.p, dcut.p, k0, k1, s));
         KK_CUDA(cudaStreamSynchronize(s));
-        cudaFree(dK);
-        cudaFree(dcut);
     }
     return KK_OK;
 }
@@ -838,6 +845,15 @@ int ensure_ccl_workspace(kk_lattice* h) {
         cudaMalloc(&h->nbig, sizeof(unsigned long long)) || cudaMalloc(&h->rep_rows, sizeof(unsigned int) * h->R) ||
         cudaMalloc(&h->row_off, sizeof(unsigned long long) * (h->R + 1))) {
         cudaGetLastError();
+        // release the partial workspace so that a later call starts over
+        void** ws[] = {(void**)&h->edges, (void**)&h->node_size, (void**)&h->node_par, (void**)&h->node_rep,
+                       (void**)&h->root_size, (void**)&h->counter, (void**)&h->open_flag, (void**)&h->compact,
+                       (void**)&h->open_count, (void**)&h->hist, (void**)&h->big, (void**)&h->nbig,
+                       (void**)&h->rep_rows, (void**)&h->row_off};
+        for (void** q : ws) {
+            cudaFree(*q);
+            *q = nullptr;
+        }
         return fail(KK_ERR_NOMEM, "cluster workspace: device allocation failed");
     }
     return KK_OK;
@@ -1003,12 +1019,11 @@ int kk_get_lattice(kk_handle h, uint8_t* out, void* stream) {
     if (!out) return fail(KK_ERR_ARG, "out is null");
     cudaStream_t s = S(stream);
     const size_t n = (size_t)h->R * h->g.rows * h->g.Lx;
-    uint8_t* tmp = nullptr;
-    KK_CUDA(cudaMalloc(&tmp, n));
-    KK_CUDA(launch_unpack(h->buf[h->cur], tmp, h->g, h->R, s));
-    KK_CUDA(cudaMemcpyAsync(out, tmp, n, cudaMemcpyDeviceToHost, s));
+    DevBuf<uint8_t> tmp;
+    KK_CUDA(tmp.alloc(n));
+    KK_CUDA(launch_unpack(h->buf[h->cur], tmp.p, h->g, h->R, s));
+    KK_CUDA(cudaMemcpyAsync(out, tmp.p, n, cudaMemcpyDeviceToHost, s));
     KK_CUDA(cudaStreamSynchronize(s));
-    cudaFree(tmp);
     return KK_OK;
 }
 
@@ -1017,12 +1032,11 @@ int kk_set_lattice(kk_handle h, const uint8_t* in, void* stream) {
     if (!in) return fail(KK_ERR_ARG, "in is null");
     cudaStream_t s = S(stream);
     const size_t n = (size_t)h->R * h->g.rows * h->g.Lx;
-    uint8_t* tmp = nullptr;
-    KK_CUDA(cudaMalloc(&tmp, n));
-    KK_CUDA(cudaMemcpyAsync(tmp, in, n, cudaMemcpyHostToDevice, s));
-    KK_CUDA(launch_pack(tmp, h->buf[h->cur], h->g, h->R, s));
+    DevBuf<uint8_t> tmp;
+    KK_CUDA(tmp.alloc(n));
+    KK_CUDA(cudaMemcpyAsync(tmp.p, in, n, cudaMemcpyHostToDevice, s));
+    KK_CUDA(launch_pack(tmp.p, h->buf[h->cur], h->g, h->R, s));
     KK_CUDA(cudaStreamSynchronize(s));
-    cudaFree(tmp);
     return KK_OK;
 }
 
