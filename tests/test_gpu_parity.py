@@ -255,3 +255,13 @@ def test_cluster_histogram_random_stress():
             for r in range(R):
                 assert got[r] == O.cluster_histogram(lat[r], target), (Lx, Ly, R, r, f, target)
         L.close()
+
+
+@pytest.mark.parametrize("tma", [1, 0])
+def test_tile_kernel_tma_staging_with_replicas(tma):
+    """Interior tiles staged by TMA boxes (3D tensor map: word, row, replica)
+    and edge tiles by LDG, with replicas, against the oracle; KK_TMA=0 forces
+    LDG staging everywhere."""
+    from paper_1309_4349_b200 import kk
+    assert kk.plan(2048, 256, replicas=3)["kernel"] == "tile"
+    _run_parity(2048, 256, 0.5, 0.7, 2048 + tma, 3, R=3, env={"KK_TMA": tma})
