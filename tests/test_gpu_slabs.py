@@ -78,7 +78,7 @@ def _run(labs, bufs, n_passes):
 
 
 @pytest.mark.parametrize("Lx,Ly,S,T,n", [(64, 96, 2, 4, 3), (72, 120, 3, 8, 2), (128, 64, 4, 2, 2),
-                                         (1024, 2048, 4, 8, 1)])
+                                         (1024, 2048, 4, 8, 1), (2048, 512, 2, 8, 2)])
 def test_slab_passes_match_whole_lattice(Lx, Ly, S, T, n):
     import os
     os.environ["KK_THI"] = "8"          # several bands per slab: interior + boundary regions both used
