@@ -1,5 +1,5 @@
 """Pass-kernel rate with TMA staging (KK_TMA=1) vs LDG staging (KK_TMA=0).
-Usage: python tools/tma_rate.py"""
+Usage: python tools/tma_rate.py [sizes...]"""
 import os
 import sys
 
@@ -10,7 +10,7 @@ from paper_1309_4349_b200 import kk  # noqa: E402
 
 torch.cuda.set_device(0)
 s = torch.cuda.current_stream()
-for L_ in (4096, 16384, 65536):
+for L_ in [int(a) for a in sys.argv[1:]] or (4096, 16384, 65536):
     line = f"{L_}^2:"
     for tma in ("0", "1", "0", "1"):
         os.environ["KK_TMA"] = tma
