@@ -88,7 +88,7 @@ int kk_create_ex(kk_handle* out, const kk_config* cfg);
  * (<= 0: query cfg->device or the current device).  The plan never changes
  * results (every kernel is bit-identical); it decides speed.
  * Honours the same environment overrides as kk_create_ex (kk_sweep). */
-enum { KK_KERNEL_TILE = 0, KK_KERNEL_RESIDENT = 1, KK_KERNEL_BAND = 2 };
+enum { KK_KERNEL_TILE = 0, KK_KERNEL_RESIDENT = 1, KK_KERNEL_BAND = 2, KK_KERNEL_CLUSTER = 3 };
 typedef struct {
     int32_t kernel;          /* KK_KERNEL_*: what kk_sweep launches */
     int32_t iters_per_pass;  /* T of the tile kernel (kk_pass always uses the tile kernel) */
@@ -117,7 +117,8 @@ int kk_destroy(kk_handle h);
  * environment overrides for testing: KK_RESIDENT=0/2 (never/always when it
  * fits), KK_BAND=2 (band kernel), KK_THI/KK_TWI (tile shape),
  * KK_RES_THREADS=128/256/512, KK_PASS_THREADS=384/512, KK_TMA=0 (LDG
- * instead of TMA staging). */
+ * instead of TMA staging), KK_CLUSTER=2/4/8/16 (cluster kernel: the band
+ * kernel inside one thread-block cluster per replica, halos over DSMEM). */
 int kk_sweep(kk_handle h, int64_t n, void* stream);
 
 /* Energy per replica (R3): nab_out[r] = N_AB (unlike nearest-neighbour pairs,

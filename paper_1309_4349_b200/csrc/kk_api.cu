@@ -46,6 +46,8 @@ int band_smem_bytes(const Geom& g, int nbands);
 void set_band_layout(BandParams& P);
 int64_t band_xch_words(const Geom& g, int nbands);
 cudaError_t launch_band(const BandParams& P, cudaStream_t stream);
+int cluster_smem_bytes(const Geom& g, int csize);
+cudaError_t launch_band_cluster(const BandParams& P, int64_t replicas, cudaStream_t stream);
 int resident_smem_bytes(const Geom& g);
 int resident_threads(const Geom& g, int64_t replicas, int nsm, int forced);
 cudaError_t launch_resident(const ResParams& P, int64_t replicas, int nt, cudaStream_t stream);
@@ -102,6 +104,7 @@ struct kk_lattice {
     int res_nt = 512;                 // its CTA size
     int pass_nt = 512;                // tile kernel CTA size (384 or 512)
     int nbands = 0;                   // > 0: kk_sweep runs the band kernel (lattice resident across all SMs)
+    int cluster_size = 0;             // > 0: kk_sweep runs the cluster kernel (one cluster per replica)
     uint32_t* xch = nullptr;          // band kernel exchange rows
     unsigned int* band_flags = nullptr;
     unsigned int* band_error = nullptr;
@@ -548,6 +551,21 @@ int plan_handle(kk_lattice* h, const kk_config* c, int T, int nsm) {
     const int bmode = env_int("KK_BAND", 0);
     const int nb = (int)std::min<int64_t>(nsm, h->g.rows / 4);
     h->nbands = (!h->resident && h->R == 1 && bmode == 2 && band_smem_bytes(h->g, nb) > 0) ? nb : 0;
+    // cluster kernel: the band kernel inside one thread-block cluster per
+    // replica, halos over DSMEM.  Auto (KK_CLUSTER unset) with 8 CTAs for a
+    // few (<= 4) replicas of a lattice that would otherwise run on one SM each
+    // and has >= 320 rows and >= 256 columns: 400^2 1.9 -> 3.5, 512^2 2.8 ->
+    // 6.1 G/s per lattice (tools/cluster_rate.py; smaller lattices lose to
+    // the per-iteration cluster barriers).  KK_CLUSTER=0 never, =2/4/8/16 forces.
+    const int cmode = env_int("KK_CLUSTER", -1);
+    int csize = cmode;
+    if (cmode < 0)
+        csize = (h->resident && h->R <= 4 && h->g.rows >= 320 && h->g.Lx >= 256) ? 8 : 0;
+    h->cluster_size = (csize > 0 && h->g.periodic && cluster_smem_bytes(h->g, csize) > 0) ? csize : 0;
+    if (h->cluster_size) {
+        h->resident = 0;
+        h->nbands = 0;
+    }
     if (pass_smem_bytes(T, h->THI, h->TWI) > 227 * 1024)
         return fail(KK_ERR_ARG, "tile too large for shared memory (KK_THI/KK_TWI)");
     return KK_OK;
@@ -580,7 +598,10 @@ int kk_plan_config(const kk_config* c, int n_sm, kk_plan* out) {
     rc = plan_handle(&tmp, c, T, n_sm);
     if (rc != KK_OK) return rc;
     *out = kk_plan{};
-    out->kernel = tmp.nbands ? KK_KERNEL_BAND : (tmp.resident ? KK_KERNEL_RESIDENT : KK_KERNEL_TILE);
+    out->kernel = tmp.cluster_size ? KK_KERNEL_CLUSTER
+                  : tmp.nbands      ? KK_KERNEL_BAND
+                  : tmp.resident    ? KK_KERNEL_RESIDENT
+                                    : KK_KERNEL_TILE;
     out->iters_per_pass = T;
     out->tile_rows = tmp.THI;
     out->tile_words = tmp.TWI;
@@ -595,10 +616,14 @@ int kk_plan_config(const kk_config* c, int n_sm, kk_plan* out) {
         out->threads = tmp.res_nt;
         out->smem_bytes = resident_smem_bytes(tmp.g);
         out->ctas = tmp.R;
-    } else {
+    } else if (out->kernel == KK_KERNEL_BAND) {
         out->threads = 1024;
         out->smem_bytes = band_smem_bytes(tmp.g, tmp.nbands);
         out->ctas = tmp.nbands;
+    } else {
+        out->threads = 256;
+        out->smem_bytes = cluster_smem_bytes(tmp.g, tmp.cluster_size);
+        out->ctas = (int64_t)tmp.cluster_size * tmp.R;
     }
     return KK_OK;
 }
@@ -712,6 +737,27 @@ int kk_sweep(kk_handle h, int64_t n, void* stream) {
     KK_CHECK_HANDLE(h);
     if (!h->g.periodic) return fail(KK_ERR_STATE, "kk_sweep: slab handle (use kk_pass)");
     if (n < 0) return fail(KK_ERR_ARG, "n must be >= 0");
+    if (h->cluster_size && n > 0) {
+        BandParams B{};
+        B.src = h->buf[h->cur];
+        B.dst = h->buf[h->cur ^ 1];
+        B.stats = h->stats;
+        B.g = h->g;
+        B.sweep0 = (uint32_t)h->sweep;
+        B.j0 = h->j;
+        B.n_iters = 16 * n;
+        const PassParams Q = make_pass_params(h, nullptr, nullptr);
+        B.key0 = Q.key0;
+        B.key1 = Q.key1;
+        for (int k = 0; k < 20; ++k) B.rk[k] = Q.rk[k];
+        for (int k = 0; k < 7; ++k) B.thr[k] = Q.thr[k];
+        B.nbands = h->cluster_size;
+        set_band_layout(B);
+        KK_CUDA(launch_band_cluster(B, h->R, S(stream)));
+        h->cur ^= 1;
+        h->sweep += n;
+        return KK_OK;
+    }
     if (h->nbands && n > 0) {
         BandParams B{};
         B.src = h->buf[h->cur];

@@ -16,9 +16,11 @@
 //  * resident_kernel<NT>: replicas that fit in one SM's shared memory; one
 //    CTA per replica runs every iteration of a kk_sweep call in place, the
 //    periodic wrap kept as rebuilt copies.
-//  * band_kernel<NT> (opt-in): one row band per SM, the whole lattice in
-//    shared memory across the GPU, 3-row halos exchanged through L2 per
-//    iteration.
+//  * band_kernel<NT, CLU>: one row band per CTA, the whole lattice in shared
+//    memory for all iterations of a call, 3-row halos exchanged per
+//    iteration — across all SMs through L2 with release/acquire flags
+//    (opt-in), or inside one thread-block cluster per replica through DSMEM
+//    (the cluster kernel, default for single mid-small lattices).
 // Everything that depends only on the tile position (global centre-octet
 // indices per word, centre-row indices per row, ownership masks) and the
 // per-pass constants (pair threshold table, pair direction table) is
@@ -36,6 +38,8 @@
 #include <cuda.h>  // CUtensorMap (TMA descriptor type only; no driver calls here)
 
 #include <algorithm>
+
+#include <cooperative_groups.h>
 
 #include "kk_internal.cuh"
 
@@ -943,10 +947,17 @@ __device__ __forceinline__ void class_rows(int ky, int lo, int hi, int& first, i
     n = hi > first ? (hi - first + 3) / 4 : 0;
 }
 
-template <int NT>
+// CLU: the bands of one replica form a thread-block cluster (nbands = cluster
+// size, one cluster per replica) and the 3-row halos are read straight from
+// the neighbouring CTAs' shared memory (DSMEM) between two cluster barriers,
+// instead of the L2 exchange buffer and flags.
+template <int NT, bool CLU>
 __global__ void __launch_bounds__(NT, 1) band_kernel(const BandParams P) {
-    const int b = blockIdx.x, nb = P.nbands;
+    const int nb = P.nbands;
+    const int b = CLU ? (int)(blockIdx.x % (unsigned)nb) : (int)blockIdx.x;
+    const int rep = CLU ? (int)(blockIdx.x / (unsigned)nb) : 0;
     const Geom& g = P.g;
+    const uint32_t* src_rep = P.src + (int64_t)rep * g.rep_words;
     const int W = g.W, tail = g.tail;
     const int y0 = band_y0(g.rows, nb, b), y1 = band_y0(g.rows, nb, b + 1);
     const int BR = y1 - y0, H = BR + 6, Wt = W + 2, WS = Wt + kCol0;
@@ -981,7 +992,7 @@ __global__ void __launch_bounds__(NT, 1) band_kernel(const BandParams P) {
     for (int i = threadIdx.x; i < H * W; i += NT) {
         const int r = i / W, x = i - r * W;
         const int64_t y = wrap_mod((int64_t)y0 - 3 + r, g.rows);
-        kk_smem[r * WS + kCol0 + 1 + x] = P.src[y * W + x];
+        kk_smem[r * WS + kCol0 + 1 + x] = src_rep[y * W + x];
     }
     __syncthreads();
     band_refresh<NT>(S, H);
@@ -999,14 +1010,14 @@ __global__ void __launch_bounds__(NT, 1) band_kernel(const BandParams P) {
     const int64_t xside = 3 * xrow, xslot = 2 * xside, xband = 2 * xslot;
 #pragma unroll 1
     while (left > 0) {
-        const Words4 sched = philox10(0u, 0u, sweep, kTagSchedule, P.key0, P.key1);
+        const Words4 sched = philox10(0u, 0u, sweep, ((uint32_t)rep << 8) | kTagSchedule, P.key0, P.key1);
         const int jend = (int)min64(16, j + left);
         left -= jend - j;
 #pragma unroll 1
         for (; j < jend; ++j) {
             const uint32_t k = ((j < 8 ? sched.a : sched.b) >> (4 * (j & 7))) & 15u;
             const int kx = (int)(k & 3u), ky = (int)(k >> 2);
-            const uint32_t c3 = (uint32_t)j;
+            const uint32_t c3 = ((uint32_t)rep << 8) | (uint32_t)j;
             // Centre rows [2, BR + 4).  Boundary rows (within 2 of a published
             // row's writers: [2, 7) and [BR - 1, BR + 4)) first; then publish;
             // then the interior rows [7, BR - 1) while the exchange is in flight.
@@ -1023,6 +1034,28 @@ __global__ void __launch_bounds__(NT, 1) band_kernel(const BandParams P) {
         default: band_iteration<3, NT>(S, R1, N1, R2, N2, sweep, c3, P.rk, acc); break;          \
     }
             KK_BAND_ITEMS(rt, nt_, rb, nb_)
+            if constexpr (CLU) {
+                KK_BAND_ITEMS(ri, ni, 0, 0)
+                acc_flush(acc);
+                namespace cg = cooperative_groups;
+                cg::cluster_group cl = cg::this_cluster();
+                cl.sync();  // every band's flips of this iteration have landed
+                // halos from the neighbours' shared memory: rows y0-3..y0-1 =
+                // up's last 3 own rows, y1..y1+2 = dn's first 3 own rows
+                const int BRu = band_y0(g.rows, nb, up + 1) - band_y0(g.rows, nb, up);
+                const uint32_t* su = cl.map_shared_rank(kk_smem, up);
+                const uint32_t* sd = cl.map_shared_rank(kk_smem, dn);
+                for (int i = threadIdx.x; i < 6 * W; i += NT) {
+                    const int k6 = i / W, x = i - k6 * W;
+                    const int lr = k6 < 3 ? k6 : BR + k6;                 // my halo rows
+                    const int rr = k6 < 3 ? BRu + k6 : 3 + (k6 - 3);       // their own rows
+                    kk_smem[lr * WS + kCol0 + 1 + x] = (k6 < 3 ? su : sd)[rr * WS + kCol0 + 1 + x];
+                }
+                cl.sync();  // nobody modifies its rows before the neighbours have read them
+                band_refresh<NT>(S, H);
+                __syncthreads();
+                continue;
+            }
             __syncthreads();
             // publish: side 0 = first 3 real rows, side 1 = last 3
             ++gi;
@@ -1090,7 +1123,7 @@ __global__ void __launch_bounds__(NT, 1) band_kernel(const BandParams P) {
     for (int i = threadIdx.x; i < BR * W; i += NT) {
         const int r = i / W, x = i - r * W;
         const uint32_t v = kk_smem[(r + 3) * WS + kCol0 + 1 + x];
-        P.dst[(int64_t)(y0 + r) * W + x] = x == W - 1 ? (v & last) : v;
+        P.dst[(int64_t)rep * g.rep_words + (int64_t)(y0 + r) * W + x] = x == W - 1 ? (v & last) : v;
     }
     if (lane == 0)
         red[3 * (NT / 32) + warp] =
@@ -1099,7 +1132,7 @@ __global__ void __launch_bounds__(NT, 1) band_kernel(const BandParams P) {
     if (threadIdx.x < 4) {
         unsigned long long s = 0;
         for (int k = 0; k < NT / 32; ++k) s += red[threadIdx.x * (NT / 32) + k];
-        if (s) atomicAdd(P.stats + threadIdx.x, s);
+        if (s) atomicAdd(P.stats + rep * 4 + threadIdx.x, s);
     }
 }
 
@@ -1208,12 +1241,12 @@ int64_t band_xch_words(const Geom& g, int nbands) { return (int64_t)nbands * 2 *
 cudaError_t launch_band(const BandParams& P, cudaStream_t stream) {
     const int smem = band_smem_bytes(P.g, P.nbands);
     if (!smem) return cudaErrorInvalidValue;
-    cudaError_t e = ensure_dynamic_smem((const void*)band_kernel<kBandThreads>, smem);
+    cudaError_t e = ensure_dynamic_smem((const void*)band_kernel<kBandThreads, false>, smem);
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(P.flags, 0, sizeof(unsigned int) * P.nbands, stream);
     if (e != cudaSuccess) return e;
     void* args[] = {const_cast<BandParams*>(&P)};
-    e = cudaLaunchCooperativeKernel((const void*)band_kernel<kBandThreads>, dim3((unsigned)P.nbands),
+    e = cudaLaunchCooperativeKernel((const void*)band_kernel<kBandThreads, false>, dim3((unsigned)P.nbands),
                                     dim3(kBandThreads), args, (size_t)smem, stream);
     if (e != cudaSuccess) return e;
     count_launch();
@@ -1228,6 +1261,44 @@ extern "C" int kk_debug_pass_clocks(unsigned long long* out) {
     return 0;
 }
 #endif
+
+// Cluster variant: one cluster of P.nbands CTAs (<= 16, 256 threads) per
+// replica, halos through DSMEM.  0 from cluster_smem_bytes if it does not fit.
+constexpr int kClusterThreads = 256;
+
+int cluster_smem_bytes(const Geom& g, int csize) {
+    if (csize != 2 && csize != 4 && csize != 8 && csize != 16) return 0;
+    Geom g2 = g;
+    return band_smem_bytes(g2, csize);
+}
+
+cudaError_t launch_band_cluster(const BandParams& P, int64_t replicas, cudaStream_t stream) {
+    const int smem = cluster_smem_bytes(P.g, P.nbands);
+    if (!smem) return cudaErrorInvalidValue;
+    const void* fn = (const void*)band_kernel<kClusterThreads, true>;
+    cudaError_t e = ensure_dynamic_smem(fn, smem);
+    if (e != cudaSuccess) return e;
+    if (P.nbands > 8) {
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(P.nbands * replicas));
+    cfg.blockDim = dim3(kClusterThreads);
+    cfg.dynamicSmemBytes = (size_t)smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)P.nbands;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, band_kernel<kClusterThreads, true>, P);
+    if (e != cudaSuccess) return e;
+    count_launch();
+    return cudaGetLastError();
+}
 
 cudaError_t launch_pass(int T, const PassParams& P, const CUtensorMap& tmap, int grid_y, int replicas,
                         cudaStream_t stream, int threads) {

@@ -43,7 +43,7 @@ class Plan(ctypes.Structure):
                 ("reserved", ctypes.c_int32), ("ctas", ctypes.c_int64)]
 
 
-KERNEL_NAMES = {0: "tile", 1: "resident", 2: "band"}
+KERNEL_NAMES = {0: "tile", 1: "resident", 2: "band", 3: "cluster"}
 
 
 # symbol -> (restype, argtypes); the ABI surface declared in include/kk.h

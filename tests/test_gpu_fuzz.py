@@ -20,7 +20,7 @@ def _configs(n=40, seed=20261018):
         Ly = int(rng.integers(1, 33)) * 4
         R = int(rng.choice([1, 1, 2, 3]))
         T = int(rng.choice([1, 2, 4, 8]))
-        path = str(rng.choice(["default", "tile", "resident", "band"]))
+        path = str(rng.choice(["default", "tile", "resident", "band", "cluster"]))
         omega = float(np.round(rng.uniform(-2.0, 3.0), 3))
         f = float(np.round(rng.uniform(0.0, 1.0), 3))
         sweeps = int(rng.integers(1, 6))
@@ -29,8 +29,9 @@ def _configs(n=40, seed=20261018):
     return out
 
 
-ENV = {"default": {}, "tile": {"KK_RESIDENT": 0, "KK_BAND": 0}, "resident": {"KK_RESIDENT": 2},
-       "band": {"KK_RESIDENT": 0, "KK_BAND": 2}}
+ENV = {"default": {}, "tile": {"KK_RESIDENT": 0, "KK_BAND": 0, "KK_CLUSTER": 0},
+       "resident": {"KK_RESIDENT": 2, "KK_CLUSTER": 0}, "band": {"KK_RESIDENT": 0, "KK_BAND": 2, "KK_CLUSTER": 0},
+       "cluster": {"KK_CLUSTER": 4}}
 
 
 @pytest.mark.parametrize("k,Lx,Ly,R,T,path,omega,f,sweeps,split", _configs())

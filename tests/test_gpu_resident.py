@@ -135,3 +135,27 @@ def test_config2_4096_band_and_tile_agree():
     ref = O.init_random(4096, 4096, 0.5, 4096)
     O.run(ref, 0.6, 4096, 3)
     assert np.array_equal(A.get_lattice()[0], ref)
+
+
+# ---- cluster kernel (opt-in): the band kernel inside one thread-block cluster
+# per replica, 3-row halos read from the neighbouring CTAs' shared memory
+@pytest.mark.parametrize("Lx,Ly,R,C", [(64, 64, 1, 16), (400, 400, 1, 16), (400, 40, 1, 8), (100, 32, 2, 8),
+                                       (128, 96, 3, 4), (68, 16, 1, 2), (1000, 64, 1, 16)])
+def test_cluster_kernel_matches_oracle(Lx, Ly, R, C):
+    _run_parity(Lx, Ly, 0.5, 0.8, Lx + Ly + C, 4, R=R, env={"KK_CLUSTER": C})
+
+
+def test_cluster_kernel_mid_sweep_start():
+    from paper_1309_4349_b200 import kk
+    Lx, Ly, seed, om = 400, 80, 555, 0.7
+    L = _lat(Lx, Ly, 0.5, om, seed, iters_per_pass=4, env={"KK_CLUSTER": 8})
+    ref = O.init_random(Lx, Ly, 0.5, seed)
+    L.run_pass(kk.REGION_ALL, None, None)      # tile kernel: iterations 0..3 of sweep 0
+    L.pass_commit()
+    L.sweep(2)                                  # cluster kernel from (sweep 0, j = 4)
+    for _ in range(3):
+        L.run_pass(kk.REGION_ALL, None, None)
+        L.pass_commit()
+    ost = O.run(ref, om, seed, 3)
+    assert np.array_equal(L.get_lattice()[0], ref)
+    assert list(L.stats()[0]) == [ost["attempted"], ost["trivial"], ost["accepted"], ost["dnab_sum"]]

@@ -18,7 +18,7 @@ def _lib():
     from paper_1309_4349_b200 import build
     build.build()
     saved = {k: os.environ.pop(k, None) for k in ("KK_RESIDENT", "KK_BAND", "KK_THI", "KK_TWI", "KK_T",
-                                                  "KK_RES_THREADS", "KK_PASS_THREADS")}
+                                                  "KK_RES_THREADS", "KK_PASS_THREADS", "KK_CLUSTER")}
     yield
     for k, v in saved.items():
         if v is not None:
@@ -41,7 +41,9 @@ def test_mid_size_lattice_fills_every_sm():
 
 def test_small_and_replica_batches_are_resident():
     assert kk.plan(64, 64)["kernel"] == "resident"
-    assert kk.plan(400, 400)["kernel"] == "resident"             # the paper's lattice
+    assert kk.plan(400, 400)["kernel"] == "cluster"              # the paper's lattice: one 8-CTA cluster
+    assert kk.plan(400, 400)["ctas"] == 8
+    assert kk.plan(400, 400, replicas=8)["kernel"] == "resident"  # enough replicas to fill SMs one each
     p = kk.plan(400, 400, replicas=1024)                           # BASELINE configs[3]
     assert p["kernel"] == "resident" and p["ctas"] == 1024 and p["threads"] == 256
     assert kk.plan(400, 400, replicas=100)["threads"] == 512     # all replicas co-resident
@@ -57,6 +59,11 @@ def test_slabs_never_use_the_resident_or_band_kernels():
 
 
 def test_overrides(monkeypatch):
+    monkeypatch.setenv("KK_CLUSTER", "0")
+    assert kk.plan(400, 400)["kernel"] == "resident"
+    monkeypatch.setenv("KK_CLUSTER", "16")
+    assert kk.plan(400, 400)["ctas"] == 16
+    monkeypatch.delenv("KK_CLUSTER")
     monkeypatch.setenv("KK_RESIDENT", "0")
     assert kk.plan(400, 400)["kernel"] == "tile"
     monkeypatch.setenv("KK_BAND", "2")
@@ -91,6 +98,8 @@ def test_plan_invariants(Lx, Ly, R, T):
         assert p["smem_bytes"] <= SMEM_2_PER_SM or os.environ.get("KK_THI")
     elif p["kernel"] == "resident":
         assert p["ctas"] == R and Lx >= 64 and p["threads"] in (128, 256, 512)
+    elif p["kernel"] == "cluster":
+        assert p["ctas"] == 8 * R and R <= 4 and Ly >= 320
 
 
 def test_invalid_configs_fail_without_a_gpu():
