@@ -167,6 +167,7 @@ struct BandParams {
     int32_t mt_off, wm_off, rl_off, th_off, dt_off, red_off;  // shared-memory layout (smem_layout)
     int32_t nbands;
     int32_t max_rows;          // rows of the largest band
+    int32_t xbuf_off;          // cluster kernel: [2 parities][6 rows][W] halo rows pushed by the neighbours
     uint32_t* xch;             // [nbands][2 slots][2 sides][3 rows][W]
     unsigned int* flags;       // [nbands]: last iteration published (1-based, zeroed per launch)
     unsigned int* error;       // set if a neighbour never published (timeout)

@@ -1035,24 +1035,40 @@ __global__ void __launch_bounds__(NT, 1) band_kernel(const BandParams P) {
     }
             KK_BAND_ITEMS(rt, nt_, rb, nb_)
             if constexpr (CLU) {
-                KK_BAND_ITEMS(ri, ni, 0, 0)
-                acc_flush(acc);
                 namespace cg = cooperative_groups;
                 cg::cluster_group cl = cg::this_cluster();
-                cl.sync();  // every band's flips of this iteration have landed
-                // halos from the neighbours' shared memory: rows y0-3..y0-1 =
-                // up's last 3 own rows, y1..y1+2 = dn's first 3 own rows
-                const int BRu = band_y0(g.rows, nb, up + 1) - band_y0(g.rows, nb, up);
-                const uint32_t* su = cl.map_shared_rank(kk_smem, up);
-                const uint32_t* sd = cl.map_shared_rank(kk_smem, dn);
+                __syncthreads();  // my first and last 3 own rows are final for this iteration
+                // push them into the neighbours' halo buffers of the next
+                // parity (they read the other parity meanwhile): up gets my
+                // first 3 rows as its bottom halo, dn my last 3 as its top halo
+                ++gi;
+                const int par = (int)(gi & 1u);
+                uint32_t* bu = cl.map_shared_rank(kk_smem + P.xbuf_off + par * 6 * W, up);
+                uint32_t* bd = cl.map_shared_rank(kk_smem + P.xbuf_off + par * 6 * W, dn);
                 for (int i = threadIdx.x; i < 6 * W; i += NT) {
                     const int k6 = i / W, x = i - k6 * W;
-                    const int lr = k6 < 3 ? k6 : BR + k6;                 // my halo rows
-                    const int rr = k6 < 3 ? BRu + k6 : 3 + (k6 - 3);       // their own rows
-                    kk_smem[lr * WS + kCol0 + 1 + x] = (k6 < 3 ? su : sd)[rr * WS + kCol0 + 1 + x];
+                    if (k6 < 3) bd[k6 * W + x] = kk_smem[(BR + k6) * WS + kCol0 + 1 + x];
+                    else bu[k6 * W + x] = kk_smem[k6 * WS + kCol0 + 1 + x];  // own rows 3..5
                 }
-                cl.sync();  // nobody modifies its rows before the neighbours have read them
-                band_refresh<NT>(S, H);
+                KK_BAND_ITEMS(ri, ni, 0, 0)
+                acc_flush(acc);
+                cl.sync();  // every push and every flip of this iteration has landed
+                // halo rows (all words, x copies included) from the buffer, and
+                // the x copies of the own rows, in one pass
+                const int xb = P.xbuf_off + par * 6 * W;
+                const int nx = tail ? 3 : 2;
+                const int n_halo = 6 * (W + 2), n_own = BR * nx;
+                for (int i = threadIdx.x; i < n_halo + n_own; i += NT) {
+                    if (i < n_halo) {
+                        const int k6 = i / (W + 2), w = i - k6 * (W + 2);
+                        const int lr = k6 < 3 ? k6 : BR + k6;  // 0..2, BR+3..BR+5
+                        kk_smem[lr * WS + kCol0 + w] = res_word(xb + k6 * W - 1, w, W, tail);
+                    } else {
+                        const int i2 = i - n_halo, a = i2 / nx, k = i2 - a * nx;
+                        const int lr = 3 + a, w = k == 0 ? 0 : (k == 1 ? W + 1 : W);
+                        kk_smem[lr * WS + kCol0 + w] = res_word(lr * WS + kCol0, w, W, tail);
+                    }
+                }
                 __syncthreads();
                 continue;
             }
@@ -1218,7 +1234,7 @@ int band_smem_bytes(const Geom& g, int nbands) {
     for (int b = 0; b < nbands; ++b) max_rows = std::max(max_rows, band_y0(g.rows, nbands, b + 1) - band_y0(g.rows, nbands, b));
     const int64_t H = max_rows + 6, Wt = g.W + 2, WS = Wt + kCol0;
     if (H * WS > 227 * 256) return 0;
-    const int64_t bytes = 4 * (int64_t)smem_layout((int)H, (int)Wt, (int)WS).words;
+    const int64_t bytes = 4 * ((int64_t)smem_layout((int)H, (int)Wt, (int)WS).words + 12 * (int64_t)g.W);
     return bytes <= 227 * 1024 ? (int)bytes : 0;
 }
 
@@ -1234,6 +1250,7 @@ void set_band_layout(BandParams& P) {
     P.th_off = L.th_off;
     P.dt_off = L.dt_off;
     P.red_off = L.red_off;
+    P.xbuf_off = (L.words + 3) & ~3;
 }
 
 int64_t band_xch_words(const Geom& g, int nbands) { return (int64_t)nbands * 2 * 2 * 3 * g.W; }
