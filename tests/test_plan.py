@@ -43,7 +43,8 @@ def test_small_and_replica_batches_are_resident():
     assert kk.plan(64, 64)["kernel"] == "resident"
     assert kk.plan(400, 400)["kernel"] == "cluster"              # the paper's lattice: one 8-CTA cluster
     assert kk.plan(400, 400)["ctas"] == 8
-    assert kk.plan(400, 400, replicas=8)["kernel"] == "resident"  # enough replicas to fill SMs one each
+    assert kk.plan(400, 400, replicas=16)["kernel"] == "cluster"  # 16 clusters of 8 CTAs fit on 148 SMs
+    assert kk.plan(400, 400, replicas=32)["kernel"] == "resident"  # enough replicas to fill SMs one each
     p = kk.plan(400, 400, replicas=1024)                           # BASELINE configs[3]
     assert p["kernel"] == "resident" and p["ctas"] == 1024 and p["threads"] == 256
     assert kk.plan(400, 400, replicas=100)["threads"] == 512     # all replicas co-resident
@@ -99,7 +100,7 @@ def test_plan_invariants(Lx, Ly, R, T):
     elif p["kernel"] == "resident":
         assert p["ctas"] == R and Lx >= 64 and p["threads"] in (128, 256, 512)
     elif p["kernel"] == "cluster":
-        assert p["ctas"] == 8 * R and R <= 4 and Ly >= 320
+        assert p["ctas"] == 8 * R and 8 * R <= 148 and Ly >= 320
 
 
 def test_invalid_configs_fail_without_a_gpu():
