@@ -552,16 +552,25 @@ int plan_handle(kk_lattice* h, const kk_config* c, int T, int nsm) {
     const int nb = (int)std::min<int64_t>(nsm, h->g.rows / 4);
     h->nbands = (!h->resident && h->R == 1 && bmode == 2 && band_smem_bytes(h->g, nb) > 0) ? nb : 0;
     // cluster kernel: the band kernel inside one thread-block cluster per
-    // replica, halos over DSMEM.  Auto (KK_CLUSTER unset) with 8 CTAs when the
-    // replicas' clusters all fit on the GPU at once (R * 8 <= #SMs) and each
-    // replica would otherwise run on one SM, with >= 320 rows and >= 256
-    // columns: 400^2 1.9 -> 3.9, 512^2 2.8 -> 7.1 G/s per lattice, 8 x 400^2
-    // 15 -> 31 G/s (tools/cluster_rate.py; smaller lattices lose to the
-    // per-iteration cluster barrier).  KK_CLUSTER=0 never, =2/4/8/16 forces.
+    // replica, halos over DSMEM.  Auto (KK_CLUSTER unset) for replicas that
+    // would otherwise run on one SM each, with >= 320 rows and >= 256 columns:
+    // the largest cluster of 8/4/2 CTAs for which all replicas' clusters fit
+    // on the GPU at once (400^2: 1 replica 1.9 -> 4.0 G/s with 8 CTAs, 18
+    // replicas 34 -> 59, 37 replicas 69 -> 88 with 4, 74 replicas 138 -> 175
+    // with 2; tools/cluster_rate.py, cluster_replicas.py, cluster_c2.py;
+    // smaller lattices lose to the per-iteration cluster barrier).
+    // KK_CLUSTER=0 never, =2/4/8/16 forces.
     const int cmode = env_int("KK_CLUSTER", -1);
     int csize = cmode;
-    if (cmode < 0)
-        csize = (h->resident && h->R * 8 <= nsm && h->g.rows >= 320 && h->g.Lx >= 256) ? 8 : 0;
+    if (cmode < 0) {
+        csize = 0;
+        if (h->resident && h->g.rows >= 320 && h->g.Lx >= 256)
+            for (int c : {8, 4, 2})
+                if (h->R * c <= nsm) {
+                    csize = c;
+                    break;
+                }
+    }
     h->cluster_size = (csize > 0 && h->g.periodic && cluster_smem_bytes(h->g, csize) > 0) ? csize : 0;
     if (h->cluster_size) {
         h->resident = 0;

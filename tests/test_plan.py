@@ -43,8 +43,10 @@ def test_small_and_replica_batches_are_resident():
     assert kk.plan(64, 64)["kernel"] == "resident"
     assert kk.plan(400, 400)["kernel"] == "cluster"              # the paper's lattice: one 8-CTA cluster
     assert kk.plan(400, 400)["ctas"] == 8
-    assert kk.plan(400, 400, replicas=16)["kernel"] == "cluster"  # 16 clusters of 8 CTAs fit on 148 SMs
-    assert kk.plan(400, 400, replicas=32)["kernel"] == "resident"  # enough replicas to fill SMs one each
+    assert kk.plan(400, 400, replicas=16)["ctas"] == 16 * 8     # 16 clusters of 8 CTAs fit on 148 SMs
+    assert kk.plan(400, 400, replicas=37)["ctas"] == 37 * 4     # then clusters of 4, of 2
+    assert kk.plan(400, 400, replicas=74)["ctas"] == 74 * 2
+    assert kk.plan(400, 400, replicas=75)["kernel"] == "resident"  # enough replicas to fill SMs one each
     p = kk.plan(400, 400, replicas=1024)                           # BASELINE configs[3]
     assert p["kernel"] == "resident" and p["ctas"] == 1024 and p["threads"] == 256
     assert kk.plan(400, 400, replicas=100)["threads"] == 512     # all replicas co-resident
@@ -100,7 +102,7 @@ def test_plan_invariants(Lx, Ly, R, T):
     elif p["kernel"] == "resident":
         assert p["ctas"] == R and Lx >= 64 and p["threads"] in (128, 256, 512)
     elif p["kernel"] == "cluster":
-        assert p["ctas"] == 8 * R and 8 * R <= 148 and Ly >= 320
+        assert p["ctas"] % R == 0 and p["ctas"] // R in (2, 4, 8) and p["ctas"] <= 148 and Ly >= 320
 
 
 def test_invalid_configs_fail_without_a_gpu():
