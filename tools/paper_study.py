@@ -35,6 +35,12 @@ def main():
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     torch.cuda.set_device(0)
+    if a.seeds > 1 and "KK_CLUSTER" not in os.environ:
+        # each handle's plan assumes it has the GPU to itself: with several
+        # replicas per handle it would take one 8-CTA cluster per replica, and
+        # 18 such handles oversubscribe the SMs; one SM per replica (resident
+        # kernel) is the better split for many concurrent handles
+        os.environ["KK_CLUSTER"] = "0"
     omegas = [0.2, 0.3, 0.4, 0.5, 0.6, 0.7, 0.8, 0.9, 1.0]
     fracs = [0.5, 0.3]
     pts = [(f, om) for f in fracs for om in omegas]
