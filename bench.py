@@ -54,6 +54,8 @@ def parse():
     p.add_argument("--no-ccl", action="store_true", help="skip the cluster histogram in the step")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-other-configs", action="store_true",
+                   help="skip the short device-timed runs of BASELINE configs[0..3] (rank 0, N=1)")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     return p.parse_args()
 
@@ -113,6 +115,31 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)),
                 "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def other_configs(torch):
+    """Short device-timed runs of the other BASELINE configs on this GPU (not
+    the headline metric; context for the per-config table in DESIGN.md)."""
+    from paper_1309_4349_b200 import kk
+    out = []
+    s = torch.cuda.current_stream()
+    for name, Lx, Ly, R, om, n in [("configs[0] 64x64", 64, 64, 1, 0.5, 1000),
+                                   ("configs[1] 400x400, one lattice", 400, 400, 1, 0.6, 1000),
+                                   ("configs[2] 4096x4096", 4096, 4096, 1, 0.6, 100),
+                                   ("configs[3] 1024 x 400x400 replicas", 400, 400, 1024, 0.6, 20)]:
+        L = kk.Lattice(Lx, Ly, 0.5, om, 7, replicas=R)
+        L.sweep(2, s)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        L.sweep(n, s)
+        e1.record(s)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        out.append({"workload": name, "kernel": kk.plan(Lx, Ly, replicas=R, n_sm=0)["kernel"], "sweeps": n,
+                    "value": n * Lx * Ly * R / (ms / 1e3), "unit": UNIT})
+        L.close()
+    return out
 
 
 def measured_peaks():
@@ -383,6 +410,8 @@ def main():
         }
         if world == 1 and not a.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(a.cpu_seconds, a.omega, a.fraction, a.seed)
+        if world == 1 and not a.no_other_configs:
+            out["other_configs"] = other_configs(torch)
         print(json.dumps(out), flush=True)
     sim.close()
     if dist:
