@@ -249,6 +249,20 @@ class Lattice:
         return [list(zip(sizes[cuts[r]:cuts[r + 1]], counts[cuts[r]:cuts[r + 1]]))
                 for r in range(self.replicas)]
 
+    def cluster_histogram_total(self, target: int = 1, stream=None):
+        """Cluster-size histogram summed over all replicas: sorted [(size, count)]
+        (the ensemble statistics of a replica batch; numpy aggregation of the
+        per-replica rows, no per-row Python work)."""
+        rows = self.cluster_histogram_raw(target, capacity=max(1 << 16, 2 * getattr(self, "_hist_rows", 0)),
+                                          stream=stream)
+        self._hist_rows = max(getattr(self, "_hist_rows", 0), len(rows))
+        if len(rows) == 0:
+            return []
+        sizes, inv = np.unique(rows[:, 1], return_inverse=True)
+        counts = np.zeros(len(sizes), np.int64)
+        np.add.at(counts, inv, rows[:, 2])
+        return list(zip(sizes.tolist(), counts.tolist()))
+
     def cluster_histogram_raw(self, target: int = 1, capacity: int = 1 << 16, stream=None):
         """Rows (replica, size, count) as an int64 array (no per-replica lists)."""
         lib = load()

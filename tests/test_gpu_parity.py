@@ -265,3 +265,16 @@ def test_tile_kernel_tma_staging_with_replicas(tma):
     from paper_1309_4349_b200 import kk
     assert kk.plan(2048, 256, replicas=3)["kernel"] == "tile"
     _run_parity(2048, 256, 0.5, 0.7, 2048 + tma, 3, R=3, env={"KK_TMA": tma})
+
+
+def test_cluster_histogram_total_over_replicas():
+    """The replica-summed histogram equals the sum of the oracle's per-replica
+    histograms (BASELINE configs[3]-style ensemble statistics)."""
+    from collections import Counter
+    L, ref = _run_parity(100, 40, 0.4, 0.9, 77, 6, R=5)
+    for target in (0, 1):
+        tot = Counter()
+        for r in range(5):
+            for sz, c in O.cluster_histogram(ref[r], target):
+                tot[sz] += c
+        assert L.cluster_histogram_total(target) == sorted(tot.items())
