@@ -48,6 +48,9 @@ int64_t band_xch_words(const Geom& g, int nbands);
 cudaError_t launch_band(const BandParams& P, cudaStream_t stream);
 int cluster_smem_bytes(const Geom& g, int csize);
 cudaError_t launch_band_cluster(const BandParams& P, int64_t replicas, cudaStream_t stream);
+int cluster_tb_smem_bytes(const Geom& g, int csize, int TB);
+void set_cluster_tb_layout(BandParams& P, int TB);
+cudaError_t launch_cluster_tb(const BandParams& P, int64_t replicas, int TB, cudaStream_t stream);
 int resident_smem_bytes(const Geom& g);
 int resident_threads(const Geom& g, int64_t replicas, int nsm, int forced);
 cudaError_t launch_resident(const ResParams& P, int64_t replicas, int nt, cudaStream_t stream);
@@ -105,6 +108,7 @@ struct kk_lattice {
     int pass_nt = 512;                // tile kernel CTA size (384 or 512)
     int nbands = 0;                   // > 0: kk_sweep runs the band kernel (lattice resident across all SMs)
     int cluster_size = 0;             // > 0: kk_sweep runs the cluster kernel (one cluster per replica)
+    int cluster_tb = 1;               // its iterations per halo exchange (1: band_kernel<256, true>)
     uint32_t* xch = nullptr;          // band kernel exchange rows
     unsigned int* band_flags = nullptr;
     unsigned int* band_error = nullptr;
@@ -551,20 +555,19 @@ int plan_handle(kk_lattice* h, const kk_config* c, int T, int nsm) {
     const int bmode = env_int("KK_BAND", 0);
     const int nb = (int)std::min<int64_t>(nsm, h->g.rows / 4);
     h->nbands = (!h->resident && h->R == 1 && bmode == 2 && band_smem_bytes(h->g, nb) > 0) ? nb : 0;
-    // cluster kernel: the band kernel inside one thread-block cluster per
-    // replica, halos over DSMEM.  Auto (KK_CLUSTER unset) for replicas that
-    // would otherwise run on one SM each, with >= 320 rows and >= 256 columns:
-    // the largest cluster of 8/4/2 CTAs for which all replicas' clusters fit
-    // on the GPU at once (400^2: 1 replica 1.9 -> 4.0 G/s with 8 CTAs, 18
-    // replicas 34 -> 59, 37 replicas 69 -> 88 with 4, 74 replicas 138 -> 175
-    // with 2; tools/cluster_rate.py, cluster_replicas.py, cluster_c2.py;
-    // smaller lattices lose to the per-iteration cluster barrier).
+    // cluster kernel: one thread-block cluster per replica, one row band per
+    // CTA, halos over DSMEM every few iterations.  Auto (KK_CLUSTER unset) for
+    // replicas that would otherwise run on one SM each, with >= 192 rows and
+    // >= 192 columns: the largest cluster of 8/4/2 CTAs for which all
+    // replicas' clusters fit on the GPU at once (400^2: 1 replica 1.9 -> 5.4
+    // G/s with 8 CTAs, 37 replicas 69 -> 107 with 4, 74 replicas 138 -> 206
+    // with 2; 256^2: 2.0 -> 3.1; tools/cluster_rate.py, cluster_c2.py).
     // KK_CLUSTER=0 never, =2/4/8/16 forces.
     const int cmode = env_int("KK_CLUSTER", -1);
     int csize = cmode;
     if (cmode < 0) {
         csize = 0;
-        if (h->resident && h->g.rows >= 320 && h->g.Lx >= 256)
+        if (h->resident && h->g.rows >= 192 && h->g.Lx >= 192)
             for (int c : {8, 4, 2})
                 if (h->R * c <= nsm) {
                     csize = c;
@@ -572,6 +575,25 @@ int plan_handle(kk_lattice* h, const kk_config* c, int T, int nsm) {
                 }
     }
     h->cluster_size = (csize > 0 && h->g.periodic && cluster_smem_bytes(h->g, csize) > 0) ? csize : 0;
+    {
+        // halo exchange every TB iterations (default 4, or 2 when the bands are
+        // too short for 3*4-row halos; KK_CLUSTER_TB=1/2/4/8 forces): 400^2 on
+        // 8 CTAs 3.9 -> 5.4 G/s, 74 x 400^2 on 2-CTA clusters 175 -> 205
+        // (tools/cluster_tb.py)
+        const int forced = env_int("KK_CLUSTER_TB", 0);
+        h->cluster_tb = 1;
+        if (h->cluster_size) {
+            if (forced > 0) {
+                if (forced == 1 || cluster_tb_smem_bytes(h->g, h->cluster_size, forced) > 0) h->cluster_tb = forced;
+            } else {
+                for (int tb : {4, 2})
+                    if (cluster_tb_smem_bytes(h->g, h->cluster_size, tb) > 0) {
+                        h->cluster_tb = tb;
+                        break;
+                    }
+            }
+        }
+    }
     if (h->cluster_size) {
         h->resident = 0;
         h->nbands = 0;
@@ -762,8 +784,13 @@ int kk_sweep(kk_handle h, int64_t n, void* stream) {
         for (int k = 0; k < 20; ++k) B.rk[k] = Q.rk[k];
         for (int k = 0; k < 7; ++k) B.thr[k] = Q.thr[k];
         B.nbands = h->cluster_size;
-        set_band_layout(B);
-        KK_CUDA(launch_band_cluster(B, h->R, S(stream)));
+        if (h->cluster_tb > 1) {
+            set_cluster_tb_layout(B, h->cluster_tb);
+            KK_CUDA(launch_cluster_tb(B, h->R, h->cluster_tb, S(stream)));
+        } else {
+            set_band_layout(B);
+            KK_CUDA(launch_band_cluster(B, h->R, S(stream)));
+        }
         h->cur ^= 1;
         h->sweep += n;
         return KK_OK;

@@ -1152,6 +1152,194 @@ __global__ void __launch_bounds__(NT, 1) band_kernel(const BandParams P) {
     }
 }
 
+
+// ---- cluster kernel with temporal blocking ------------------------------------
+// One thread-block cluster per replica, one row band per CTA (as the cluster
+// variant of band_kernel), but halos of HY = 3*TB rows exchanged once every
+// TB iterations (R8): between exchanges each CTA advances its band plus the
+// shrinking light cone of its halos on its own, so the cluster barrier, the
+// DSMEM pushes and the halo rebuild are paid once per TB iterations.  The
+// rows processed in each iteration follow the exact light cone of the
+// block's remaining classes, as in the tile kernel.  Local row lr holds
+// y = y0 - HY + lr.
+template <int NT, int TB>
+__global__ void __launch_bounds__(NT, 1) cluster_kernel(const BandParams P) {
+    namespace cg = cooperative_groups;
+    constexpr int HY = 3 * TB;
+    const int nb = P.nbands;
+    const int b = (int)(blockIdx.x % (unsigned)nb), rep = (int)(blockIdx.x / (unsigned)nb);
+    const Geom& g = P.g;
+    const int W = g.W, tail = g.tail;
+    const int y0 = band_y0(g.rows, nb, b), y1 = band_y0(g.rows, nb, b + 1);
+    const int BR = y1 - y0, H = BR + 2 * HY, Wt = W + 2, WS = Wt + kCol0;
+    const int up = b == 0 ? nb - 1 : b - 1, dn = b + 1 == nb ? 0 : b + 1;
+    const uint32_t* src = P.src + (int64_t)rep * g.rep_words;
+    Tabs S;
+    S.WS = WS;
+    S.Lx = (uint32_t)g.Lx;
+    S.rW = W;
+    S.rTail = tail;
+    S.rRows = BR;
+    S.mt_off = P.mt_off;
+    S.wm_off = P.wm_off;
+    S.rl_off = P.rl_off;
+    S.th_off = P.th_off;
+    S.dt_off = P.dt_off;
+    unsigned long long* red = reinterpret_cast<unsigned long long*>(kk_smem + P.red_off);
+    uint2* thr2 = reinterpret_cast<uint2*>(kk_smem + S.th_off);
+    uint2* mtab = reinterpret_cast<uint2*>(kk_smem + S.mt_off);
+    for (int i = threadIdx.x; i < 256; i += NT) thr2[i] = make_uint2(P.thr[min(i & 15, 6)], P.thr[min(i >> 4, 6)]);
+    fill_dir_table<NT>(S);
+    for (int w = threadIdx.x; w < Wt; w += NT) {
+        mtab[w] = make_uint2(w >= 1 ? 32u * (uint32_t)(w - 1) : 0u, 1u);
+        uint32_t own = 0;
+        if (w >= 1 && w <= W) own = (w == W && tail) ? ((1u << tail) - 1u) : 0xFFFFFFFFu;
+        kk_smem[S.wm_off + w] = own;
+    }
+    for (int r = threadIdx.x; r < H; r += NT) {
+        const int64_t y = wrap_mod((int64_t)y0 - HY + r, g.rows);
+        kk_smem[S.rl_off + r] = (uint32_t)(y >> 2) | ((r >= HY && r < HY + BR) ? 0x80000000u : 0u);
+    }
+    for (int i = threadIdx.x; i < H * W; i += NT) {
+        const int r = i / W, x = i - r * W;
+        const int64_t y = wrap_mod((int64_t)y0 - HY + r, g.rows);
+        kk_smem[r * WS + kCol0 + 1 + x] = src[y * W + x];
+    }
+    __syncthreads();
+    band_refresh<NT>(S, H);
+    __syncthreads();
+
+    cg::cluster_group cl = cg::this_cluster();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0)
+        for (int k = 0; k < 4; ++k) red[k * (NT / 32) + warp] = 0ull;
+    Acc acc = {0u, 0u, 0u, 0u, 0u, 0ull};
+    uint32_t sweep = P.sweep0;
+    int j = P.j0;
+    int64_t left = P.n_iters;
+    int blk = 0;
+    const int phase = HY & 3;  // local row lr holds class ky iff (lr - HY) % 4 == ky
+#pragma unroll 1
+    while (left > 0) {
+        const int tb = (int)min64(TB, left);
+        // the block's classes (it may span two sweeps)
+        uint32_t ks[TB];
+        uint32_t sw[TB];
+        int js[TB];
+        {
+            uint32_t s2 = sweep;
+            int j2 = j;
+            Words4 sc = philox10(0u, 0u, s2, ((uint32_t)rep << 8) | kTagSchedule, P.key0, P.key1);
+#pragma unroll
+            for (int t = 0; t < TB; ++t) {
+                ks[t] = ((j2 < 8 ? sc.a : sc.b) >> (4 * (j2 & 7))) & 15u;
+                sw[t] = s2;
+                js[t] = j2;
+                if (++j2 == 16) {
+                    j2 = 0;
+                    ++s2;
+                    sc = philox10(0u, 0u, s2, ((uint32_t)rep << 8) | kTagSchedule, P.key0, P.key1);
+                }
+            }
+        }
+#pragma unroll 1
+        for (int t = 0; t < tb; ++t) {
+            const int kx = (int)(ks[t] & 3u), ky = (int)(ks[t] >> 2);
+            const uint32_t c3 = ((uint32_t)rep << 8) | (uint32_t)js[t];
+            // exact light cone of the block's remaining iterations
+            int a = HY, bb = HY + BR;
+#pragma unroll
+            for (int u = TB - 1; u > 0; --u) {
+                if (u <= t || u >= tb) continue;
+                const int ph = ((int)(ks[u] >> 2) + phase) & 3;
+                const int cmin = (a - 1) + ((ph - (a - 1)) & 3);
+                const int cmax = bb - ((bb - ph) & 3);
+                if (cmin <= cmax) {
+                    a = min(a, cmin - 2);
+                    bb = max(bb, cmax + 3);
+                }
+            }
+            const int r_lo = max(2, a - 1), r_hi = min(H - 2, bb + 1);
+            const int ph = (ky + phase) & 3;
+            const int r_first = r_lo + ((ph - r_lo) & 3);
+            const int nrows = r_hi > r_first ? (r_hi - r_first + 3) / 4 : 0;
+            switch (kx) {
+                case 0: band_iteration<0, NT>(S, r_first, nrows, 0, 0, sw[t], c3, P.rk, acc); break;
+                case 1: band_iteration<1, NT>(S, r_first, nrows, 0, 0, sw[t], c3, P.rk, acc); break;
+                case 2: band_iteration<2, NT>(S, r_first, nrows, 0, 0, sw[t], c3, P.rk, acc); break;
+                default: band_iteration<3, NT>(S, r_first, nrows, 0, 0, sw[t], c3, P.rk, acc); break;
+            }
+            acc_flush(acc);
+            __syncthreads();
+            band_refresh<NT>(S, H);
+            __syncthreads();
+        }
+        j += tb;
+        while (j >= 16) {
+            j -= 16;
+            ++sweep;
+        }
+        left -= tb;
+        // counters of this block (<= TB iterations: 32-bit sums per warp cannot overflow)
+        {
+            uint32_t c0 = acc.attempted, c1 = acc.trivial, c2 = acc.accepted, c3s = (uint32_t)acc.idx_sum;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                c0 += __shfl_xor_sync(0xFFFFFFFFu, c0, o);
+                c1 += __shfl_xor_sync(0xFFFFFFFFu, c1, o);
+                c2 += __shfl_xor_sync(0xFFFFFFFFu, c2, o);
+                c3s += __shfl_xor_sync(0xFFFFFFFFu, c3s, o);
+            }
+            if (lane == 0) {
+                red[0 * (NT / 32) + warp] += c0;
+                red[1 * (NT / 32) + warp] += c1;
+                red[2 * (NT / 32) + warp] += c2;
+                red[3 * (NT / 32) + warp] += c3s;
+            }
+            acc.attempted = acc.trivial = acc.accepted = 0u;
+            acc.idx_sum = 0ull;
+        }
+        if (left <= 0) break;
+        // exchange: push my first / last HY own rows into the neighbours'
+        // buffers of this block's parity, one cluster barrier, rebuild halos
+        ++blk;
+        const int par = blk & 1;
+        uint32_t* bu = cl.map_shared_rank(kk_smem + P.xbuf_off + par * 2 * HY * W, up);
+        uint32_t* bd = cl.map_shared_rank(kk_smem + P.xbuf_off + par * 2 * HY * W, dn);
+        for (int i = threadIdx.x; i < 2 * HY * W; i += NT) {
+            const int k = i / W, x = i - k * W;
+            if (k < HY) bd[k * W + x] = kk_smem[(BR + k) * WS + kCol0 + 1 + x];   // my last HY own rows
+            else bu[k * W + x] = kk_smem[k * WS + kCol0 + 1 + x];                    // my first HY own rows
+        }
+        cl.sync();
+        const int xb = P.xbuf_off + par * 2 * HY * W;
+        for (int i = threadIdx.x; i < 2 * HY * (W + 2); i += NT) {
+            const int k = i / (W + 2), w = i - k * (W + 2);
+            const int lr = k < HY ? k : BR + k;  // 0..HY-1, BR+HY..BR+2HY-1
+            kk_smem[lr * WS + kCol0 + w] = res_word(xb + k * W - 1, w, W, tail);
+        }
+        __syncthreads();
+    }
+
+    // write back the band's own rows
+    const uint32_t last = tail ? ((1u << tail) - 1u) : 0xFFFFFFFFu;
+    uint32_t* dst = P.dst + (int64_t)rep * g.rep_words;
+    for (int i = threadIdx.x; i < BR * W; i += NT) {
+        const int r = i / W, x = i - r * W;
+        const uint32_t v = kk_smem[(r + HY) * WS + kCol0 + 1 + x];
+        dst[(int64_t)(y0 + r) * W + x] = x == W - 1 ? (v & last) : v;
+    }
+    if (lane == 0)
+        red[3 * (NT / 32) + warp] =
+            (unsigned long long)(2 * ((long long)red[3 * (NT / 32) + warp] - 3 * (long long)red[2 * (NT / 32) + warp]));
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        unsigned long long sum = 0;
+        for (int k = 0; k < NT / 32; ++k) sum += red[threadIdx.x * (NT / 32) + k];
+        if (sum) atomicAdd(P.stats + rep * 4 + threadIdx.x, sum);
+    }
+}
+
 }  // namespace
 
 int pass_smem_bytes(int T, int THI, int TWI) {
@@ -1312,6 +1500,72 @@ cudaError_t launch_band_cluster(const BandParams& P, int64_t replicas, cudaStrea
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     e = cudaLaunchKernelEx(&cfg, band_kernel<kClusterThreads, true>, P);
+    if (e != cudaSuccess) return e;
+    count_launch();
+    return cudaGetLastError();
+}
+
+// Temporally blocked cluster kernel: halos of 3*TB rows exchanged every TB
+// iterations.  0 if it does not fit (every band needs >= 3*TB rows).
+int cluster_tb_smem_bytes(const Geom& g, int csize, int TB) {
+    if (csize != 2 && csize != 4 && csize != 8 && csize != 16) return 0;
+    if (TB != 2 && TB != 4 && TB != 8) return 0;
+    if (g.Lx < 64 || (g.tail && g.W < 3) || !g.periodic || g.rows / 4 < csize) return 0;
+    int max_rows = 0, min_rows = 1 << 30;
+    for (int b = 0; b < csize; ++b) {
+        const int br = band_y0(g.rows, csize, b + 1) - band_y0(g.rows, csize, b);
+        max_rows = std::max(max_rows, br);
+        min_rows = std::min(min_rows, br);
+    }
+    if (min_rows < 3 * TB) return 0;
+    const int64_t H = max_rows + 6 * TB, Wt = g.W + 2, WS = Wt + kCol0;
+    if (H * WS > 227 * 256) return 0;
+    const int64_t words = ((int64_t)smem_layout((int)H, (int)Wt, (int)WS).words + 3) / 4 * 4 + 2 * 6 * TB * (int64_t)g.W;
+    return 4 * words <= 227 * 1024 ? (int)(4 * words) : 0;
+}
+
+void set_cluster_tb_layout(BandParams& P, int TB) {
+    int max_rows = 0;
+    for (int b = 0; b < P.nbands; ++b)
+        max_rows = std::max(max_rows, band_y0(P.g.rows, P.nbands, b + 1) - band_y0(P.g.rows, P.nbands, b));
+    P.max_rows = max_rows;
+    const SmemLayout L = smem_layout(max_rows + 6 * TB, P.g.W + 2, P.g.W + 2 + kCol0);
+    P.mt_off = L.mt_off;
+    P.wm_off = L.wm_off;
+    P.rl_off = L.rl_off;
+    P.th_off = L.th_off;
+    P.dt_off = L.dt_off;
+    P.red_off = L.red_off;
+    P.xbuf_off = (L.words + 3) & ~3;
+}
+
+cudaError_t launch_cluster_tb(const BandParams& P, int64_t replicas, int TB, cudaStream_t stream) {
+    const int smem = cluster_tb_smem_bytes(P.g, P.nbands, TB);
+    if (!smem) return cudaErrorInvalidValue;
+    const void* fn = TB == 2   ? (const void*)cluster_kernel<kClusterThreads, 2>
+                     : TB == 4 ? (const void*)cluster_kernel<kClusterThreads, 4>
+                               : (const void*)cluster_kernel<kClusterThreads, 8>;
+    cudaError_t e = ensure_dynamic_smem(fn, smem);
+    if (e != cudaSuccess) return e;
+    if (P.nbands > 8) {
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(P.nbands * replicas));
+    cfg.blockDim = dim3(kClusterThreads);
+    cfg.dynamicSmemBytes = (size_t)smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)P.nbands;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (TB == 2) e = cudaLaunchKernelEx(&cfg, cluster_kernel<kClusterThreads, 2>, P);
+    else if (TB == 4) e = cudaLaunchKernelEx(&cfg, cluster_kernel<kClusterThreads, 4>, P);
+    else e = cudaLaunchKernelEx(&cfg, cluster_kernel<kClusterThreads, 8>, P);
     if (e != cudaSuccess) return e;
     count_launch();
     return cudaGetLastError();

@@ -159,3 +159,30 @@ def test_cluster_kernel_mid_sweep_start():
     ost = O.run(ref, om, seed, 3)
     assert np.array_equal(L.get_lattice()[0], ref)
     assert list(L.stats()[0]) == [ost["attempted"], ost["trivial"], ost["accepted"], ost["dnab_sum"]]
+
+
+@pytest.mark.parametrize("tb", [2, 4, 8])
+@pytest.mark.parametrize("Lx,Ly,R,C", [(400, 400, 1, 8), (100, 96, 2, 4), (256, 512, 1, 16), (1000, 96, 1, 2)])
+def test_cluster_kernel_temporal_blocking(Lx, Ly, R, C, tb):
+    """Halos of 3*TB rows exchanged every TB iterations (KK_CLUSTER_TB)."""
+    from paper_1309_4349_b200 import kk
+    rows_per_band = Ly // C
+    if rows_per_band < 3 * tb + 4:
+        pytest.skip("bands too short for this TB")
+    _run_parity(Lx, Ly, 0.5, 0.8, Lx + Ly + C + tb, 5, R=R, env={"KK_CLUSTER": C, "KK_CLUSTER_TB": tb})
+
+
+def test_cluster_kernel_temporal_blocking_mid_sweep():
+    from paper_1309_4349_b200 import kk
+    Lx, Ly, seed, om = 400, 160, 556, 0.7
+    L = _lat(Lx, Ly, 0.5, om, seed, iters_per_pass=4, env={"KK_CLUSTER": 4, "KK_CLUSTER_TB": 4})
+    ref = O.init_random(Lx, Ly, 0.5, seed)
+    L.run_pass(kk.REGION_ALL, None, None)      # tile kernel: iterations 0..3 of sweep 0
+    L.pass_commit()
+    L.sweep(2)                                  # cluster kernel from (sweep 0, j = 4), blocks across sweeps
+    for _ in range(3):
+        L.run_pass(kk.REGION_ALL, None, None)
+        L.pass_commit()
+    ost = O.run(ref, om, seed, 3)
+    assert np.array_equal(L.get_lattice()[0], ref)
+    assert list(L.stats()[0]) == [ost["attempted"], ost["trivial"], ost["accepted"], ost["dnab_sum"]]

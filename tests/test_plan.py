@@ -18,7 +18,7 @@ def _lib():
     from paper_1309_4349_b200 import build
     build.build()
     saved = {k: os.environ.pop(k, None) for k in ("KK_RESIDENT", "KK_BAND", "KK_THI", "KK_TWI", "KK_T",
-                                                  "KK_RES_THREADS", "KK_PASS_THREADS", "KK_CLUSTER")}
+                                                  "KK_RES_THREADS", "KK_PASS_THREADS", "KK_CLUSTER", "KK_CLUSTER_TB")}
     yield
     for k, v in saved.items():
         if v is not None:
@@ -102,7 +102,7 @@ def test_plan_invariants(Lx, Ly, R, T):
     elif p["kernel"] == "resident":
         assert p["ctas"] == R and Lx >= 64 and p["threads"] in (128, 256, 512)
     elif p["kernel"] == "cluster":
-        assert p["ctas"] % R == 0 and p["ctas"] // R in (2, 4, 8) and p["ctas"] <= 148 and Ly >= 320
+        assert p["ctas"] % R == 0 and p["ctas"] // R in (2, 4, 8) and p["ctas"] <= 148 and Ly >= 192
 
 
 def test_invalid_configs_fail_without_a_gpu():
