@@ -19,8 +19,10 @@
 //  * band_kernel<NT, CLU>: one row band per CTA, the whole lattice in shared
 //    memory for all iterations of a call, 3-row halos exchanged per
 //    iteration — across all SMs through L2 with release/acquire flags
-//    (opt-in), or inside one thread-block cluster per replica through DSMEM
-//    (the cluster kernel, default for single mid-small lattices).
+//    (opt-in), or inside one thread-block cluster per replica through DSMEM.
+//  * cluster_kernel<NT, TB>: the cluster variant with 3*TB-row halos pushed
+//    over DSMEM once every TB iterations (default for single or few
+//    mid-small lattices).
 // Everything that depends only on the tile position (global centre-octet
 // indices per word, centre-row indices per row, ownership masks) and the
 // per-pass constants (pair threshold table, pair direction table) is
