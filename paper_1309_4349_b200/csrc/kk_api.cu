@@ -51,6 +51,9 @@ cudaError_t launch_band_cluster(const BandParams& P, int64_t replicas, cudaStrea
 int cluster_tb_smem_bytes(const Geom& g, int csize, int TB);
 void set_cluster_tb_layout(BandParams& P, int TB);
 cudaError_t launch_cluster_tb(const BandParams& P, int64_t replicas, int TB, cudaStream_t stream);
+int band_tb_smem_bytes(const Geom& g, int nbands, int TB);
+int64_t band_tb_xch_words(const Geom& g, int nbands, int TB);
+cudaError_t launch_band_tb(const BandParams& P, int TB, cudaStream_t stream);
 int resident_smem_bytes(const Geom& g);
 int resident_threads(const Geom& g, int64_t replicas, int nsm, int forced);
 cudaError_t launch_resident(const ResParams& P, int64_t replicas, int nt, cudaStream_t stream);
@@ -109,6 +112,7 @@ struct kk_lattice {
     int nbands = 0;                   // > 0: kk_sweep runs the band kernel (lattice resident across all SMs)
     int cluster_size = 0;             // > 0: kk_sweep runs the cluster kernel (one cluster per replica)
     int cluster_tb = 1;               // its iterations per halo exchange (1: band_kernel<256, true>)
+    int band_tb = 1;                  // band kernel iterations per L2 halo exchange (1: band_kernel<1024, false>)
     uint32_t* xch = nullptr;          // band kernel exchange rows
     unsigned int* band_flags = nullptr;
     unsigned int* band_error = nullptr;
@@ -552,9 +556,19 @@ int plan_handle(kk_lattice* h, const kk_config* c, int T, int nsm) {
     // shared memory.  Opt-in (KK_BAND=2): measured on B200 it loses to the
     // tile kernel below ~8192^2 and wins only ~3% at 12288^2 (the L2
     // handshake per iteration costs ~3 us, tools/band_vs_tile.py).
-    const int bmode = env_int("KK_BAND", 0);
+    // With halos exchanged every 4 iterations (KK_BAND_TB, 3*TB-row halos)
+    // it beats the tile kernel from ~8192^2 until the bands no longer fit in
+    // shared memory (8192^2: 330 -> 351 G/s, 12288^2: 400 -> 418;
+    // tools/band_tb.py), so that range uses it by default (KK_BAND=0 off).
+    const int bmode = env_int("KK_BAND", -1);
     const int nb = (int)std::min<int64_t>(nsm, h->g.rows / 4);
-    h->nbands = (!h->resident && h->R == 1 && bmode == 2 && band_smem_bytes(h->g, nb) > 0) ? nb : 0;
+    const bool band_auto = bmode < 0 && h->g.rows >= 48 * (int64_t)nb && h->g.Lx >= 8192 &&
+                           band_tb_smem_bytes(h->g, nb, 4) > 0;
+    h->nbands = (!h->resident && h->R == 1 && (bmode == 2 || band_auto) && band_smem_bytes(h->g, nb) > 0) ? nb : 0;
+    {
+        const int tb = env_int("KK_BAND_TB", band_auto ? 4 : 1);
+        h->band_tb = (h->nbands && tb > 1 && band_tb_smem_bytes(h->g, nb, tb) > 0) ? tb : 1;
+    }
     // cluster kernel: one thread-block cluster per replica, one row band per
     // CTA, halos over DSMEM every few iterations.  Auto (KK_CLUSTER unset) for
     // replicas that would otherwise run on one SM each, with >= 192 rows and
@@ -686,7 +700,8 @@ int kk_create_ex(kk_handle* out, const kk_config* c) {
     cudaError_t e3 = cudaMalloc(&h->stats, sizeof(unsigned long long) * 4 * h->R);
     cudaError_t e4 = cudaMalloc(&h->obs, sizeof(unsigned long long) * 2 * h->R);
     if (h->nbands && !e4) {
-        e4 = cudaMalloc(&h->xch, 4 * band_xch_words(h->g, h->nbands));
+        e4 = cudaMalloc(&h->xch, 4 * std::max(band_xch_words(h->g, h->nbands),
+                                              band_tb_xch_words(h->g, h->nbands, h->band_tb)));
         if (!e4) e4 = cudaMalloc(&h->band_flags, sizeof(unsigned int) * h->nbands);
         if (!e4) e4 = cudaMalloc(&h->band_error, sizeof(unsigned int));
         if (!e4) e4 = cudaMemset(h->band_error, 0, sizeof(unsigned int));
@@ -813,8 +828,13 @@ int kk_sweep(kk_handle h, int64_t n, void* stream) {
         B.xch = h->xch;
         B.flags = h->band_flags;
         B.error = h->band_error;
-        set_band_layout(B);
-        KK_CUDA(launch_band(B, S(stream)));
+        if (h->band_tb > 1) {
+            set_cluster_tb_layout(B, h->band_tb);
+            KK_CUDA(launch_band_tb(B, h->band_tb, S(stream)));
+        } else {
+            set_band_layout(B);
+            KK_CUDA(launch_band(B, S(stream)));
+        }
         h->cur ^= 1;
         h->sweep += n;
         return KK_OK;

@@ -1164,12 +1164,16 @@ __global__ void __launch_bounds__(NT, 1) band_kernel(const BandParams P) {
 // rows processed in each iteration follow the exact light cone of the
 // block's remaining classes, as in the tile kernel.  Local row lr holds
 // y = y0 - HY + lr.
-template <int NT, int TB>
+// L2X: the same scheme across all SMs (one band per SM, cooperative launch,
+// one replica): the halos go through the L2 exchange buffer with release /
+// acquire flags, as in band_kernel, but once every TB iterations.
+template <int NT, int TB, bool L2X>
 __global__ void __launch_bounds__(NT, 1) cluster_kernel(const BandParams P) {
     namespace cg = cooperative_groups;
     constexpr int HY = 3 * TB;
     const int nb = P.nbands;
-    const int b = (int)(blockIdx.x % (unsigned)nb), rep = (int)(blockIdx.x / (unsigned)nb);
+    const int b = L2X ? (int)blockIdx.x : (int)(blockIdx.x % (unsigned)nb);
+    const int rep = L2X ? 0 : (int)(blockIdx.x / (unsigned)nb);
     const Geom& g = P.g;
     const int W = g.W, tail = g.tail;
     const int y0 = band_y0(g.rows, nb, b), y1 = band_y0(g.rows, nb, b + 1);
@@ -1211,7 +1215,6 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(const BandParams P) {
     band_refresh<NT>(S, H);
     __syncthreads();
 
-    cg::cluster_group cl = cg::this_cluster();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (lane == 0)
         for (int k = 0; k < 4; ++k) red[k * (NT / 32) + warp] = 0ull;
@@ -1306,6 +1309,39 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(const BandParams P) {
         // buffers of this block's parity, one cluster barrier, rebuild halos
         ++blk;
         const int par = blk & 1;
+        if constexpr (L2X) {
+            // publish side 0 = my first HY own rows, side 1 = my last HY
+            uint32_t* xo = P.xch + ((int64_t)b * 2 + par) * 2 * HY * W;
+            for (int i = threadIdx.x; i < 2 * HY * W; i += NT) {
+                const int k = i / W, x = i - k * W;
+                xo[k * W + x] = kk_smem[(k < HY ? HY + k : BR + (k - HY)) * WS + kCol0 + 1 + x];
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                st_release(P.flags + b, (unsigned)blk);
+                long long spins = 0;
+                while (ld_acquire(P.flags + up) < (unsigned)blk || ld_acquire(P.flags + dn) < (unsigned)blk) {
+                    if (++spins > (1ll << 28)) {  // a neighbour never arrived: give up loudly
+                        atomicExch(P.error, 1u);
+                        break;
+                    }
+                }
+            }
+            __syncthreads();
+            // top halo = up's last HY rows, bottom halo = dn's first HY rows
+            const uint32_t* xu = P.xch + ((int64_t)up * 2 + par) * 2 * HY * W + HY * W;
+            const uint32_t* xd = P.xch + ((int64_t)dn * 2 + par) * 2 * HY * W;
+            for (int i = threadIdx.x; i < 2 * HY * W; i += NT) {
+                const int k = i / W, x = i - k * W;
+                const int lr = k < HY ? k : BR + k;
+                kk_smem[lr * WS + kCol0 + 1 + x] = __ldcg((k < HY ? xu + k * W : xd + (k - HY) * W) + x);
+            }
+            __syncthreads();
+            band_refresh<NT>(S, H);
+            __syncthreads();
+            continue;
+        }
+        cg::cluster_group cl = cg::this_cluster();
         uint32_t* bu = cl.map_shared_rank(kk_smem + P.xbuf_off + par * 2 * HY * W, up);
         uint32_t* bd = cl.map_shared_rank(kk_smem + P.xbuf_off + par * 2 * HY * W, dn);
         for (int i = threadIdx.x; i < 2 * HY * W; i += NT) {
@@ -1544,9 +1580,9 @@ void set_cluster_tb_layout(BandParams& P, int TB) {
 cudaError_t launch_cluster_tb(const BandParams& P, int64_t replicas, int TB, cudaStream_t stream) {
     const int smem = cluster_tb_smem_bytes(P.g, P.nbands, TB);
     if (!smem) return cudaErrorInvalidValue;
-    const void* fn = TB == 2   ? (const void*)cluster_kernel<kClusterThreads, 2>
-                     : TB == 4 ? (const void*)cluster_kernel<kClusterThreads, 4>
-                               : (const void*)cluster_kernel<kClusterThreads, 8>;
+    const void* fn = TB == 2   ? (const void*)cluster_kernel<kClusterThreads, 2, false>
+                     : TB == 4 ? (const void*)cluster_kernel<kClusterThreads, 4, false>
+                               : (const void*)cluster_kernel<kClusterThreads, 8, false>;
     cudaError_t e = ensure_dynamic_smem(fn, smem);
     if (e != cudaSuccess) return e;
     if (P.nbands > 8) {
@@ -1565,9 +1601,45 @@ cudaError_t launch_cluster_tb(const BandParams& P, int64_t replicas, int TB, cud
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (TB == 2) e = cudaLaunchKernelEx(&cfg, cluster_kernel<kClusterThreads, 2>, P);
-    else if (TB == 4) e = cudaLaunchKernelEx(&cfg, cluster_kernel<kClusterThreads, 4>, P);
-    else e = cudaLaunchKernelEx(&cfg, cluster_kernel<kClusterThreads, 8>, P);
+    if (TB == 2) e = cudaLaunchKernelEx(&cfg, cluster_kernel<kClusterThreads, 2, false>, P);
+    else if (TB == 4) e = cudaLaunchKernelEx(&cfg, cluster_kernel<kClusterThreads, 4, false>, P);
+    else e = cudaLaunchKernelEx(&cfg, cluster_kernel<kClusterThreads, 8, false>, P);
+    if (e != cudaSuccess) return e;
+    count_launch();
+    return cudaGetLastError();
+}
+
+// Band kernel with temporal blocking (L2 exchange every TB iterations).
+int band_tb_smem_bytes(const Geom& g, int nbands, int TB) {
+    if (TB != 2 && TB != 4 && TB != 8) return 0;
+    if (g.Lx < 64 || (g.tail && g.W < 3) || !g.periodic || nbands < 2 || g.rows / 4 < nbands) return 0;
+    int max_rows = 0, min_rows = 1 << 30;
+    for (int b = 0; b < nbands; ++b) {
+        const int br = band_y0(g.rows, nbands, b + 1) - band_y0(g.rows, nbands, b);
+        max_rows = std::max(max_rows, br);
+        min_rows = std::min(min_rows, br);
+    }
+    if (min_rows < 3 * TB) return 0;
+    const int64_t H = max_rows + 6 * TB, Wt = g.W + 2, WS = Wt + kCol0;
+    if (H * WS > 227 * 256) return 0;
+    const int64_t bytes = 4 * (int64_t)smem_layout((int)H, (int)Wt, (int)WS).words;
+    return bytes <= 227 * 1024 ? (int)bytes : 0;
+}
+
+int64_t band_tb_xch_words(const Geom& g, int nbands, int TB) { return (int64_t)nbands * 2 * 2 * 3 * TB * g.W; }
+
+cudaError_t launch_band_tb(const BandParams& P, int TB, cudaStream_t stream) {
+    const int smem = band_tb_smem_bytes(P.g, P.nbands, TB);
+    if (!smem) return cudaErrorInvalidValue;
+    const void* fn = TB == 2   ? (const void*)cluster_kernel<kBandThreads, 2, true>
+                     : TB == 4 ? (const void*)cluster_kernel<kBandThreads, 4, true>
+                               : (const void*)cluster_kernel<kBandThreads, 8, true>;
+    cudaError_t e = ensure_dynamic_smem(fn, smem);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(P.flags, 0, sizeof(unsigned int) * P.nbands, stream);
+    if (e != cudaSuccess) return e;
+    void* args[] = {const_cast<BandParams*>(&P)};
+    e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)P.nbands), dim3(kBandThreads), args, (size_t)smem, stream);
     if (e != cudaSuccess) return e;
     count_launch();
     return cudaGetLastError();

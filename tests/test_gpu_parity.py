@@ -278,3 +278,11 @@ def test_cluster_histogram_total_over_replicas():
             for sz, c in O.cluster_histogram(ref[r], target):
                 tot[sz] += c
         assert L.cluster_histogram_total(target) == sorted(tot.items())
+
+
+def test_8192_band_kernel_default():
+    """8192^2 runs on the band kernel (halos through L2 every 4 iterations)
+    by default; one full sweep must equal the oracle."""
+    from paper_1309_4349_b200 import kk
+    assert kk.plan(8192, 8192, n_sm=0)["kernel"] == "band"
+    _run_parity(8192, 8192, 0.5, 0.6, 8192, 1)

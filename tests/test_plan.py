@@ -18,7 +18,8 @@ def _lib():
     from paper_1309_4349_b200 import build
     build.build()
     saved = {k: os.environ.pop(k, None) for k in ("KK_RESIDENT", "KK_BAND", "KK_THI", "KK_TWI", "KK_T",
-                                                  "KK_RES_THREADS", "KK_PASS_THREADS", "KK_CLUSTER", "KK_CLUSTER_TB")}
+                                                  "KK_RES_THREADS", "KK_PASS_THREADS", "KK_CLUSTER", "KK_CLUSTER_TB",
+                                                  "KK_BAND_TB")}
     yield
     for k, v in saved.items():
         if v is not None:
@@ -37,6 +38,9 @@ def test_bench_lattice_plan():
 def test_mid_size_lattice_fills_every_sm():
     p = kk.plan(4096, 4096)
     assert p["kernel"] == "tile" and p["ctas"] >= 148 and p["threads"] == 512
+    q = kk.plan(8192, 8192)                      # band kernel: one band per SM, L2 halos every 4 iterations
+    assert q["kernel"] == "band" and q["ctas"] == 148 and q["threads"] == 1024
+    assert kk.plan(16384, 16384)["kernel"] == "tile"   # bands no longer fit in shared memory
 
 
 def test_small_and_replica_batches_are_resident():
@@ -72,6 +76,8 @@ def test_overrides(monkeypatch):
     monkeypatch.setenv("KK_BAND", "2")
     assert kk.plan(4096, 4096)["kernel"] == "band"
     assert kk.plan(4096, 4096)["ctas"] == 148
+    monkeypatch.setenv("KK_BAND", "0")
+    assert kk.plan(8192, 8192)["kernel"] == "tile"
     monkeypatch.delenv("KK_BAND")
     monkeypatch.delenv("KK_RESIDENT")
     monkeypatch.setenv("KK_THI", "64")
