@@ -199,3 +199,12 @@ def test_band_kernel_temporal_blocking(Lx, Ly, tb):
         pytest.skip("bands too short for this TB")
     _run_parity(Lx, Ly, 0.5, 0.7, Lx + tb, 2, env={"KK_RESIDENT": 0, "KK_CLUSTER": 0, "KK_BAND": 2,
                                                     "KK_BAND_TB": tb})
+
+
+def test_cluster_default_for_replica_batch():
+    """16 replicas of 400^2 run on 16 eight-CTA clusters by default (128 SMs);
+    every replica must equal the oracle."""
+    from paper_1309_4349_b200 import kk
+    p = kk.plan(400, 400, replicas=16, n_sm=0)
+    assert p["kernel"] == "cluster" and p["ctas"] == 128
+    _run_parity(400, 400, 0.5, 0.7, 16, 2, R=16)
