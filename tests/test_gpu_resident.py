@@ -208,3 +208,25 @@ def test_cluster_default_for_replica_batch():
     p = kk.plan(400, 400, replicas=16, n_sm=0)
     assert p["kernel"] == "cluster" and p["ctas"] == 128
     _run_parity(400, 400, 0.5, 0.7, 16, 2, R=16)
+
+
+@pytest.mark.parametrize("Lx,Ly,env", [(512, 448, {"KK_CLUSTER": 4, "KK_CLUSTER_TB": 8}),
+                                        (128, 3584, {"KK_RESIDENT": 0, "KK_CLUSTER": 0, "KK_BAND": 2,
+                                                     "KK_BAND_TB": 8})])
+def test_temporal_blocks_spanning_two_sweeps(Lx, Ly, env):
+    """Blocks of 8 iterations starting at j = 4 cover iterations 12..15 of one
+    sweep and 0..3 of the next (schedules of two sweeps in one block); the
+    band case has 148 bands of 24 rows, the shortest that hold 3*8-row halos."""
+    from paper_1309_4349_b200 import kk
+    seed, om = 918, 0.75
+    L = _lat(Lx, Ly, 0.5, om, seed, iters_per_pass=4, env=env)
+    ref = O.init_random(Lx, Ly, 0.5, seed)
+    L.run_pass(kk.REGION_ALL, None, None)      # tile kernel: iterations 0..3 of sweep 0
+    L.pass_commit()
+    L.sweep(2)                                  # blocks 4..11, 12..3, 4..11, 12..3
+    for _ in range(3):
+        L.run_pass(kk.REGION_ALL, None, None)
+        L.pass_commit()
+    ost = O.run(ref, om, seed, 3)
+    assert np.array_equal(L.get_lattice()[0], ref)
+    assert list(L.stats()[0]) == [ost["attempted"], ost["trivial"], ost["accepted"], ost["dnab_sum"]]
