@@ -81,3 +81,28 @@ def test_two_ranks_on_one_gpu_match_the_oracle(Lx, Ly, T, n):
     assert obs["trivial"] == [st["trivial"]] and obs["dnab_sum"] == [st["dnab_sum"]]
     assert obs["clusters_A"] == sum(c for _, c in O.cluster_histogram(ref, 1))
     assert [tuple(r) for r in obs["hist0"]] == O.cluster_histogram(ref, 0)
+
+
+def test_bench_two_ranks_functional():
+    """bench.py's N>1 path end to end (torchrun, 2 ranks sharing one GPU over
+    gloo; KK_BENCH_BACKEND / KK_BENCH_DEVICE exist for exactly this check):
+    one JSON line from rank 0 with the contract's keys.  Numbers from such a
+    run are meaningless and never reported."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, KK_BENCH_BACKEND="gloo", KK_BENCH_DEVICE="0")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(root, "bench.py"),
+           "--gpus", "2", "--steps", "1", "--warmup", "1", "--Lx", "2048", "--rows-per-gpu", "1024",
+           "--sweeps-per-step", "2", "--no-other-configs"]
+    r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0
+    assert d["config"]["parallelism"] == "slab2"
+    assert d["e2e"]["h2d_bytes_per_step"] == 2 * 2048 * 1024 // 8
+    assert d["observables"]["n_a"] == [2048 * 2048 // 2]
