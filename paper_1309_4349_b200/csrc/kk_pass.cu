@@ -1093,7 +1093,7 @@ __global__ void __launch_bounds__(NT, 1) band_kernel(const BandParams P) {
             if (threadIdx.x == 0) {
                 long long spins = 0;
                 while (ld_acquire(P.flags + up) < gi || ld_acquire(P.flags + dn) < gi) {
-                    if (++spins > (1ll << 28)) {  // a neighbour never arrived: give up loudly
+                    if (++spins > (1ll << 24)) {  // a neighbour never arrived (~1 s): give up loudly
                         atomicExch(P.error, 1u);
                         break;
                     }
@@ -1321,7 +1321,7 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(const BandParams P) {
                 st_release(P.flags + b, (unsigned)blk);
                 long long spins = 0;
                 while (ld_acquire(P.flags + up) < (unsigned)blk || ld_acquire(P.flags + dn) < (unsigned)blk) {
-                    if (++spins > (1ll << 28)) {  // a neighbour never arrived: give up loudly
+                    if (++spins > (1ll << 24)) {  // a neighbour never arrived (~1 s): give up loudly
                         atomicExch(P.error, 1u);
                         break;
                     }
