@@ -188,15 +188,10 @@ def test_cluster_kernel_temporal_blocking_mid_sweep():
     assert list(L.stats()[0]) == [ost["attempted"], ost["trivial"], ost["accepted"], ost["dnab_sum"]]
 
 
-@pytest.mark.parametrize("tb", [2, 4, 8])
-@pytest.mark.parametrize("Lx,Ly", [(2048, 1024), (400, 400), (4096, 4096)])
+@pytest.mark.parametrize("Lx,Ly,tb", [(4096, 4096, 2), (4096, 4096, 4), (128, 3584, 8), (2048, 2048, 2)])
 def test_band_kernel_temporal_blocking(Lx, Ly, tb):
-    """Band kernel with 3*TB-row halos exchanged through L2 every TB iterations."""
-    from paper_1309_4349_b200 import kk
-    if kk.plan(Lx, Ly, n_sm=0)["kernel"] == "tile" and Ly // 4 < 148:
-        pytest.skip("fewer rows than bands")
-    if (Ly // min(148, Ly // 4)) < 3 * tb + 4:
-        pytest.skip("bands too short for this TB")
+    """Band kernel with 3*TB-row halos exchanged through L2 every TB iterations
+    (148 bands; 2048^2 has 13-14-row bands, 3584 rows give 24-row bands)."""
     _run_parity(Lx, Ly, 0.5, 0.7, Lx + tb, 2, env={"KK_RESIDENT": 0, "KK_CLUSTER": 0, "KK_BAND": 2,
                                                     "KK_BAND_TB": tb})
 
