@@ -202,18 +202,23 @@ def test_config2_4096x4096_one_sweep():
     _run_parity(4096, 4096, 0.5, 0.6, 123, 1)
 
 
-def test_bench_lattice_65536_window_and_invariants():
-    """BASELINE configs[4] lattice (65536 x 65536, what bench.py times):
-    invariants over the whole lattice + sampled window parity for one pass."""
+@pytest.mark.parametrize("T,init", [(4, "block"), (8, "random")])
+def test_bench_lattice_65536_window_and_invariants(T, init):
+    """BASELINE configs[4] lattice (65536 x 65536, what bench.py times; T = 8
+    with the random start is bench.py's own launch configuration: tile
+    kernel, cost-model tiles, 384-thread CTAs, TMA staging): invariants over
+    the whole lattice + sampled window parity for one pass."""
     from paper_1309_4349_b200 import kk
     Lx = Ly = 65536
-    L = _lat(Lx, Ly, 0.5, 0.6, 99, init=kk.KK_INIT_BLOCK, iters_per_pass=4)
+    L = _lat(Lx, Ly, 0.5, 0.6, 99, init=kk.KK_INIT_BLOCK if init == "block" else kk.KK_INIT_RANDOM,
+             iters_per_pass=T)
+    pl = kk.plan(Lx, Ly, iters_per_pass=T)
+    assert pl["kernel"] == "tile" and (T != 8 or pl["threads"] == 384)
     nA = L.composition()[0]
     assert nA == Lx * Ly // 2
     L.sweep(1)                                    # mix the block start
     nab0 = L.energy()[0][0]
     L.stats(reset=True)
-    T = 4
     hy = 3 * T
     before = L.get_packed()[0]
     s = L.sweep_index()
@@ -224,7 +229,7 @@ def test_bench_lattice_65536_window_and_invariants():
     nab1 = L.energy()[0][0]
     assert L.composition()[0] == nA
     assert nab1 - nab0 == st[3]
-    assert st[0] == Lx * Ly // 4                 # T=4 iterations x N/16 centres
+    assert st[0] == T * (Lx * Ly // 16)          # T iterations x N/16 centres
     rng = np.random.default_rng(5)
     for y0 in [0, Ly - 8, int(rng.integers(16, Ly - 16))]:
         H = 8
@@ -234,6 +239,41 @@ def test_bench_lattice_65536_window_and_invariants():
         exp = win[hy:hy + H]
         got = inputs.unpack_rows(after[[(y0 + r) % Ly for r in range(H)]], Lx)
         assert np.array_equal(got, exp)
+
+
+def test_bench_lattice_65536_cluster_histogram():
+    """The cluster histogram at the bench lattice size (65536 x 65536, the CCL
+    launch configuration bench.py times), checked through a lattice whose
+    clusters are known from a small oracle run: a random 256 x 256 tile with
+    a B frame (row 0, column 0) inside an A ring (rows 1 and 255, columns 1
+    and 255), repeated 256 x 256 times.  No A cluster and no interior B
+    cluster can leave its tile (every neighbour step out of a tile lands on
+    the frame or crosses it), so the big histogram is the tile's oracle
+    histogram with every count x 65536, except that the frames of all tiles
+    join into ONE B cluster of 511 x 65536 sites."""
+    from paper_1309_4349_b200 import kk
+    t, reps = 256, 256
+    tile = inputs.random_lattice(t, t, 0.5, seed=4242)
+    tile[1, :] = tile[t - 1, :] = 1
+    tile[:, 1] = tile[:, t - 1] = 1
+    tile[0, :] = 0
+    tile[:, 0] = 0
+    Lx = Ly = t * reps
+    packed_tile = np.packbits(tile, axis=1, bitorder="little").view(np.uint32)  # bit x%32 of word x/32
+    assert packed_tile.shape == (t, t // 32)
+    big = np.tile(packed_tile, (reps, reps))[None]
+    L = _lat(Lx, Ly, 0.5, 0.6, 1, init=kk.KK_INIT_EMPTY)
+    L.set_packed(np.ascontiguousarray(big))
+    del big
+    assert np.array_equal(inputs.unpack_rows(L.get_packed()[0][:t, :t // 32], t), tile)
+    n = reps * reps
+    exp_a = [(sz, c * n) for sz, c in O.cluster_histogram(tile, 1)]
+    hb = dict(O.cluster_histogram(tile, 0))
+    hb[511] -= 1                                  # the frame on the tile torus
+    exp_b = sorted([(sz, c * n) for sz, c in hb.items() if c] + [(511 * n, 1)])
+    assert L.cluster_histogram(1)[0] == exp_a
+    assert L.cluster_histogram(0)[0] == exp_b
+    L.close()
 
 
 def test_cluster_histogram_random_stress():

@@ -94,3 +94,25 @@ def test_translation_invariance():
     ref = O.cluster_histogram(lat, 1)
     for sy, sx in [(1, 0), (0, 5), (7, 11)]:
         assert O.cluster_histogram(np.roll(np.roll(lat, sy, 0), sx, 1), 1) == ref
+
+
+def test_framed_tile_tiling_rule():
+    """The rule test_gpu_parity's 65536^2 cluster test relies on, checked by
+    brute force on a 3 x 2 tiling: a tile with a B frame (row 0, column 0)
+    inside an A ring (rows 1, t-1, columns 1, t-1) keeps every A cluster and
+    every interior B cluster inside its tile, and the frames join into one B
+    cluster."""
+    from tests import inputs
+    t = 64
+    tile = inputs.random_lattice(t, t, 0.5, seed=4242)
+    tile[1, :] = tile[t - 1, :] = 1
+    tile[:, 1] = tile[:, t - 1] = 1
+    tile[0, :] = 0
+    tile[:, 0] = 0
+    big = np.tile(tile, (2, 3))
+    n = 6
+    assert O.cluster_histogram(big, 1) == [(sz, c * n) for sz, c in O.cluster_histogram(tile, 1)]
+    hb = dict(O.cluster_histogram(tile, 0))
+    frame = 2 * t - 1
+    hb[frame] -= 1
+    assert O.cluster_histogram(big, 0) == sorted([(sz, c * n) for sz, c in hb.items() if c] + [(frame * n, 1)])
