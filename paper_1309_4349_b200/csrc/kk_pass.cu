@@ -910,21 +910,37 @@ __device__ __forceinline__ void band_refresh(const Tabs& S, int H) {
     const int W = S.rW, tail = S.rTail, WS = S.WS;
     const int nx = tail ? 3 : 2;  // rewritten words of every row: 0, W+1 (and W)
     for (int i = threadIdx.x; i < H * nx; i += NT) {
-        const int r = i / nx, k = i - r * nx;
+        // i / nx without a runtime division (floor(i/3) = umulhi(i, ceil(2^32/3)) for i < 2^31)
+        const int r = tail ? (int)__umulhi((uint32_t)i, 0x55555556u) : (i >> 1), k = i - r * nx;
         const int w = k == 0 ? 0 : (k == 1 ? W + 1 : W);
         kk_smem[r * WS + kCol0 + w] = res_word(r * WS + kCol0, w, W, tail);
     }
 }
 
 // Items of the centre rows r1 + 4a (a < n1) and r2 + 4a (a < n2).
+// A thread's walk over a (rows x W) grid in steps of NT: start (a0, w0) and
+// step (da, dw), computed once per kernel so the loops issue no division.
+struct Walk {
+    int a0, w0, da, dw;
+};
+template <int NT>
+__device__ __forceinline__ Walk make_walk(int W) {
+    Walk k;
+    k.a0 = (int)threadIdx.x / W;
+    k.w0 = (int)threadIdx.x - k.a0 * W;
+    k.da = NT / W;
+    k.dw = NT - k.da * W;
+    return k;
+}
+
 template <int KX, int NT>
-__device__ __forceinline__ void band_iteration(const Tabs& S, int r1, int n1, int r2, int n2, uint32_t sweep,
-                                               uint32_t c3, const uint32_t* rk, Acc& acc) {
+__device__ __forceinline__ void band_iteration(const Tabs& S, const Walk& wk, int r1, int n1, int r2, int n2,
+                                               uint32_t sweep, uint32_t c3, const uint32_t* rk, Acc& acc) {
     const int W = S.rW;
     const int items = (n1 + n2) * W;
-    int a = threadIdx.x / W;
-    int w = threadIdx.x - a * W;
-    const int da = NT / W, dw = NT - da * W;
+    int a = wk.a0;
+    int w = wk.w0;
+    const int da = wk.da, dw = wk.dw;
     int since_flush = 0;
     for (int it = threadIdx.x; it < items; it += NT) {
         const int r = a < n1 ? r1 + 4 * a : r2 + 4 * (a - n1);
@@ -975,6 +991,7 @@ __global__ void __launch_bounds__(NT, 1) band_kernel(const BandParams P) {
     S.rl_off = P.rl_off;
     S.th_off = P.th_off;
     S.dt_off = P.dt_off;
+    const Walk wk = make_walk<NT>(W);
     unsigned long long* red = reinterpret_cast<unsigned long long*>(kk_smem + P.red_off);
     uint2* thr2 = reinterpret_cast<uint2*>(kk_smem + S.th_off);
     uint2* mtab = reinterpret_cast<uint2*>(kk_smem + S.mt_off);
@@ -1030,10 +1047,10 @@ __global__ void __launch_bounds__(NT, 1) band_kernel(const BandParams P) {
             class_rows(ky, bt_hi, bb_lo, ri, ni);
 #define KK_BAND_ITEMS(R1, N1, R2, N2)                                                             \
     switch (kx) {                                                                                 \
-        case 0: band_iteration<0, NT>(S, R1, N1, R2, N2, sweep, c3, P.rk, acc); break;           \
-        case 1: band_iteration<1, NT>(S, R1, N1, R2, N2, sweep, c3, P.rk, acc); break;           \
-        case 2: band_iteration<2, NT>(S, R1, N1, R2, N2, sweep, c3, P.rk, acc); break;           \
-        default: band_iteration<3, NT>(S, R1, N1, R2, N2, sweep, c3, P.rk, acc); break;          \
+        case 0: band_iteration<0, NT>(S, wk, R1, N1, R2, N2, sweep, c3, P.rk, acc); break;           \
+        case 1: band_iteration<1, NT>(S, wk, R1, N1, R2, N2, sweep, c3, P.rk, acc); break;           \
+        case 2: band_iteration<2, NT>(S, wk, R1, N1, R2, N2, sweep, c3, P.rk, acc); break;           \
+        default: band_iteration<3, NT>(S, wk, R1, N1, R2, N2, sweep, c3, P.rk, acc); break;          \
     }
             KK_BAND_ITEMS(rt, nt_, rb, nb_)
             if constexpr (CLU) {
@@ -1167,8 +1184,12 @@ __global__ void __launch_bounds__(NT, 1) band_kernel(const BandParams P) {
 // L2X: the same scheme across all SMs (one band per SM, cooperative launch,
 // one replica): the halos go through the L2 exchange buffer with release /
 // acquire flags, as in band_kernel, but once every TB iterations.
+// <= 128 registers at 256 threads: two CTAs fit an SM, which lets the
+// scheduler place every cluster of a replica batch at once even where a GPC's
+// SM count is not a multiple of the cluster size (37 x 400^2 at C = 4 lost
+// 17% at 155 registers).
 template <int NT, int TB, bool L2X>
-__global__ void __launch_bounds__(NT, 1) cluster_kernel(const BandParams P) {
+__global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) cluster_kernel(const BandParams P) {
     namespace cg = cooperative_groups;
     constexpr int HY = 3 * TB;
     const int nb = P.nbands;
@@ -1191,6 +1212,7 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(const BandParams P) {
     S.rl_off = P.rl_off;
     S.th_off = P.th_off;
     S.dt_off = P.dt_off;
+    const Walk wk = make_walk<NT>(W), wk2 = make_walk<NT>(W + 2);
     unsigned long long* red = reinterpret_cast<unsigned long long*>(kk_smem + P.red_off);
     uint2* thr2 = reinterpret_cast<uint2*>(kk_smem + S.th_off);
     uint2* mtab = reinterpret_cast<uint2*>(kk_smem + S.mt_off);
@@ -1247,15 +1269,17 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(const BandParams P) {
                 }
             }
         }
-#pragma unroll 1
-        for (int t = 0; t < tb; ++t) {
-            const int kx = (int)(ks[t] & 3u), ky = (int)(ks[t] >> 2);
-            const uint32_t c3 = ((uint32_t)rep << 8) | (uint32_t)js[t];
-            // exact light cone of the block's remaining iterations
+        // per iteration of the block: class, rows of the exact light cone of
+        // the block's remaining iterations, sweep and c3 — computed here with
+        // compile-time indices so the arrays stay in registers (a runtime
+        // index in the loop below would put them in local memory)
+        int rf[TB], nr[TB];
+#pragma unroll
+        for (int t = 0; t < TB; ++t) {
             int a = HY, bb = HY + BR;
 #pragma unroll
-            for (int u = TB - 1; u > 0; --u) {
-                if (u <= t || u >= tb) continue;
+            for (int u = TB - 1; u > t; --u) {
+                if (u >= tb) continue;
                 const int ph = ((int)(ks[u] >> 2) + phase) & 3;
                 const int cmin = (a - 1) + ((ph - (a - 1)) & 3);
                 const int cmax = bb - ((bb - ph) & 3);
@@ -1265,14 +1289,30 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(const BandParams P) {
                 }
             }
             const int r_lo = max(2, a - 1), r_hi = min(H - 2, bb + 1);
-            const int ph = (ky + phase) & 3;
-            const int r_first = r_lo + ((ph - r_lo) & 3);
-            const int nrows = r_hi > r_first ? (r_hi - r_first + 3) / 4 : 0;
+            const int ph = ((int)(ks[t] >> 2) + phase) & 3;
+            rf[t] = r_lo + ((ph - r_lo) & 3);
+            nr[t] = r_hi > rf[t] ? (r_hi - rf[t] + 3) / 4 : 0;
+        }
+#pragma unroll 1
+        for (int t = 0; t < tb; ++t) {
+            uint32_t kst = ks[0], swt = sw[0];
+            int jst = js[0], r_first = rf[0], nrows = nr[0];
+#pragma unroll
+            for (int u = 1; u < TB; ++u)
+                if (t == u) {
+                    kst = ks[u];
+                    swt = sw[u];
+                    jst = js[u];
+                    r_first = rf[u];
+                    nrows = nr[u];
+                }
+            const int kx = (int)(kst & 3u);
+            const uint32_t c3 = ((uint32_t)rep << 8) | (uint32_t)jst;
             switch (kx) {
-                case 0: band_iteration<0, NT>(S, r_first, nrows, 0, 0, sw[t], c3, P.rk, acc); break;
-                case 1: band_iteration<1, NT>(S, r_first, nrows, 0, 0, sw[t], c3, P.rk, acc); break;
-                case 2: band_iteration<2, NT>(S, r_first, nrows, 0, 0, sw[t], c3, P.rk, acc); break;
-                default: band_iteration<3, NT>(S, r_first, nrows, 0, 0, sw[t], c3, P.rk, acc); break;
+                case 0: band_iteration<0, NT>(S, wk, r_first, nrows, 0, 0, swt, c3, P.rk, acc); break;
+                case 1: band_iteration<1, NT>(S, wk, r_first, nrows, 0, 0, swt, c3, P.rk, acc); break;
+                case 2: band_iteration<2, NT>(S, wk, r_first, nrows, 0, 0, swt, c3, P.rk, acc); break;
+                default: band_iteration<3, NT>(S, wk, r_first, nrows, 0, 0, swt, c3, P.rk, acc); break;
             }
             acc_flush(acc);
             __syncthreads();
@@ -1344,17 +1384,33 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(const BandParams P) {
         cg::cluster_group cl = cg::this_cluster();
         uint32_t* bu = cl.map_shared_rank(kk_smem + P.xbuf_off + par * 2 * HY * W, up);
         uint32_t* bd = cl.map_shared_rank(kk_smem + P.xbuf_off + par * 2 * HY * W, dn);
-        for (int i = threadIdx.x; i < 2 * HY * W; i += NT) {
-            const int k = i / W, x = i - k * W;
-            if (k < HY) bd[k * W + x] = kk_smem[(BR + k) * WS + kCol0 + 1 + x];   // my last HY own rows
-            else bu[k * W + x] = kk_smem[k * WS + kCol0 + 1 + x];                    // my first HY own rows
+        {
+            int k = wk.a0, x = wk.w0;
+            for (int i = threadIdx.x; i < 2 * HY * W; i += NT) {
+                if (k < HY) bd[k * W + x] = kk_smem[(BR + k) * WS + kCol0 + 1 + x];   // my last HY own rows
+                else bu[k * W + x] = kk_smem[k * WS + kCol0 + 1 + x];                    // my first HY own rows
+                k += wk.da;
+                x += wk.dw;
+                if (x >= W) {
+                    x -= W;
+                    ++k;
+                }
+            }
         }
         cl.sync();
         const int xb = P.xbuf_off + par * 2 * HY * W;
-        for (int i = threadIdx.x; i < 2 * HY * (W + 2); i += NT) {
-            const int k = i / (W + 2), w = i - k * (W + 2);
-            const int lr = k < HY ? k : BR + k;  // 0..HY-1, BR+HY..BR+2HY-1
-            kk_smem[lr * WS + kCol0 + w] = res_word(xb + k * W - 1, w, W, tail);
+        {
+            int k = wk2.a0, w = wk2.w0;
+            for (int i = threadIdx.x; i < 2 * HY * (W + 2); i += NT) {
+                const int lr = k < HY ? k : BR + k;  // 0..HY-1, BR+HY..BR+2HY-1
+                kk_smem[lr * WS + kCol0 + w] = res_word(xb + k * W - 1, w, W, tail);
+                k += wk2.da;
+                w += wk2.dw;
+                if (w >= W + 2) {
+                    w -= W + 2;
+                    ++k;
+                }
+            }
         }
         __syncthreads();
     }
