@@ -700,6 +700,21 @@ __device__ __forceinline__ uint32_t res_word(int base, int w, int W, int tail) {
     return kk_smem[base + w];
 }
 
+// A thread's walk over a (rows x W) grid in steps of NT: start (a0, w0) and
+// step (da, dw), computed once per kernel so the loops issue no division.
+struct Walk {
+    int a0, w0, da, dw;
+};
+template <int NT>
+__device__ __forceinline__ Walk make_walk(int W) {
+    Walk k;
+    k.a0 = (int)threadIdx.x / W;
+    k.w0 = (int)threadIdx.x - k.a0 * W;
+    k.da = NT / W;
+    k.dw = NT - k.da * W;
+    return k;
+}
+
 template <int NT>
 __device__ __forceinline__ void res_refresh(const Tabs& S) {
     const int W = S.rW, tail = S.rTail, rows = S.rRows, WS = S.WS;
@@ -708,11 +723,13 @@ __device__ __forceinline__ void res_refresh(const Tabs& S) {
     for (int i = threadIdx.x; i < total; i += NT) {
         int dst_row, src_row, w;
         if (i < n_real) {
-            const int a = i / nx, k = i - a * nx;
+            // i / nx without a runtime division (floor(i/3) = umulhi(i, ceil(2^32/3)) for i < 2^31)
+            const int a = tail ? (int)__umulhi((uint32_t)i, 0x55555556u) : (i >> 1), k = i - a * nx;
             dst_row = src_row = 2 + a;
             w = k == 0 ? 0 : (k == 1 ? W + 1 : W);
         } else {
-            const int i2 = i - n_real, gi = i2 / (W + 2);
+            const int i2 = i - n_real;
+            const int gi = (i2 >= W + 2) + (i2 >= 2 * (W + 2)) + (i2 >= 3 * (W + 2));  // i2 / (W + 2), i2 < 4 (W + 2)
             w = i2 - gi * (W + 2);
             dst_row = gi < 2 ? gi : rows + gi;      // 0, 1, rows+2, rows+3
             src_row = gi < 2 ? rows + gi : gi;      // rows, rows+1, 2, 3
@@ -724,13 +741,13 @@ __device__ __forceinline__ void res_refresh(const Tabs& S) {
 }
 
 template <int KX, int NT>
-__device__ __forceinline__ void res_iteration(const Tabs& S, int r_first, uint32_t sweep, uint32_t c3,
-                                              const uint32_t* rk, Acc& acc) {
+__device__ __forceinline__ void res_iteration(const Tabs& S, const Walk& wk, int r_first, uint32_t sweep,
+                                              uint32_t c3, const uint32_t* rk, Acc& acc) {
     const int W = S.rW;
     const int items = (S.rRows / 4) * W;
-    int a = threadIdx.x / W;
-    int w = threadIdx.x - a * W;
-    const int da = NT / W, dw = NT - da * W;
+    int a = wk.a0;
+    int w = wk.w0;
+    const int da = wk.da, dw = wk.dw;
     if (items <= 40 * NT) {  // no byte-lane overflow before the flush after the iteration
         for (int it = threadIdx.x; it < items; it += NT) {
             process_item<KX, 1, true>(S, r_first + 4 * a, w + 1, sweep, c3, rk, acc);
@@ -776,6 +793,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) resident_kernel(const ResParams
     S.rl_off = P.rl_off;
     S.th_off = P.th_off;
     S.dt_off = P.dt_off;
+    const Walk wk = make_walk<NT>(S.rW);
     unsigned long long* red = reinterpret_cast<unsigned long long*>(kk_smem + P.red_off);
     uint2* thr2 = reinterpret_cast<uint2*>(kk_smem + S.th_off);
     uint2* mtab = reinterpret_cast<uint2*>(kk_smem + S.mt_off);
@@ -822,10 +840,10 @@ __global__ void __launch_bounds__(NT, 1024 / NT) resident_kernel(const ResParams
             const int kx = (int)(k & 3u), ky = (int)(k >> 2);
             const uint32_t c3 = ((uint32_t)rep << 8) | (uint32_t)j;
             switch (kx) {
-                case 0: res_iteration<0, NT>(S, 2 + ky, sweep, c3, P.rk, acc); break;
-                case 1: res_iteration<1, NT>(S, 2 + ky, sweep, c3, P.rk, acc); break;
-                case 2: res_iteration<2, NT>(S, 2 + ky, sweep, c3, P.rk, acc); break;
-                default: res_iteration<3, NT>(S, 2 + ky, sweep, c3, P.rk, acc); break;
+                case 0: res_iteration<0, NT>(S, wk, 2 + ky, sweep, c3, P.rk, acc); break;
+                case 1: res_iteration<1, NT>(S, wk, 2 + ky, sweep, c3, P.rk, acc); break;
+                case 2: res_iteration<2, NT>(S, wk, 2 + ky, sweep, c3, P.rk, acc); break;
+                default: res_iteration<3, NT>(S, wk, 2 + ky, sweep, c3, P.rk, acc); break;
             }
             acc_flush(acc);
             __syncthreads();
@@ -918,21 +936,6 @@ __device__ __forceinline__ void band_refresh(const Tabs& S, int H) {
 }
 
 // Items of the centre rows r1 + 4a (a < n1) and r2 + 4a (a < n2).
-// A thread's walk over a (rows x W) grid in steps of NT: start (a0, w0) and
-// step (da, dw), computed once per kernel so the loops issue no division.
-struct Walk {
-    int a0, w0, da, dw;
-};
-template <int NT>
-__device__ __forceinline__ Walk make_walk(int W) {
-    Walk k;
-    k.a0 = (int)threadIdx.x / W;
-    k.w0 = (int)threadIdx.x - k.a0 * W;
-    k.da = NT / W;
-    k.dw = NT - k.da * W;
-    return k;
-}
-
 template <int KX, int NT>
 __device__ __forceinline__ void band_iteration(const Tabs& S, const Walk& wk, int r1, int n1, int r2, int n2,
                                                uint32_t sweep, uint32_t c3, const uint32_t* rk, Acc& acc) {
