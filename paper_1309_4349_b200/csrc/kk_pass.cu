@@ -406,14 +406,29 @@ __device__ __forceinline__ void process_item(const Tabs& S, int r, int w, uint32
     acc.idx_odd += (Sg >> 4) & 0x0F0F0F0Fu;
 }
 
+// A thread's walk over a (rows x W) grid in steps of NT: start (a0, w0) and
+// step (da, dw), computed once per kernel so the loops issue no division.
+struct Walk {
+    int a0, w0, da, dw;
+};
+template <int NT>
+__device__ __forceinline__ Walk make_walk(int W) {
+    Walk k;
+    k.a0 = (int)threadIdx.x / W;
+    k.w0 = (int)threadIdx.x - k.a0 * W;
+    k.da = NT / W;
+    k.dw = NT - k.da * W;
+    return k;
+}
+
 template <int KX, bool FAST, int NT>
-__device__ __forceinline__ void run_iteration(const Tabs& S, int Wt, int r_first, int nrows, uint32_t sweep,
-                                              uint32_t c3, const uint32_t* rk, Acc& acc) {
+__device__ __forceinline__ void run_iteration(const Tabs& S, int Wt, const Walk& wk, int r_first, int nrows,
+                                              uint32_t sweep, uint32_t c3, const uint32_t* rk, Acc& acc) {
     const int items = nrows * Wt;
     // flattened (row, word) walk without per-item division
-    int a = threadIdx.x / Wt;
-    int w = threadIdx.x - a * Wt;
-    const int da = NT / Wt, dw = NT - da * Wt;
+    int a = wk.a0;
+    int w = wk.w0;
+    const int da = wk.da, dw = wk.dw;
     if (items <= 40 * NT) {
         // at most 40 items per thread: the byte-lane sums (<= 6 per item)
         // cannot overflow before the caller's flush after the iteration
@@ -578,6 +593,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks)
     const Words4 sched = philox10(0u, 0u, P.sweep, ((uint32_t)rep << 8) | kTagSchedule, P.key0, P.key1);
     Acc acc = {0u, 0u, 0u, 0u, 0u, 0ull};
     const int phase0 = (int)((Y0 - HY + g.y_begin) & 3);
+    const Walk wk = make_walk<NT>(Wt);
 
 #pragma unroll 1
     for (int t = 0; t < T; ++t) {
@@ -611,10 +627,10 @@ __global__ void __launch_bounds__(NT, kMinBlocks)
         const int r_first = r_lo + ((phase - r_lo) & 3);
         const int nrows = r_hi > r_first ? (r_hi - r_first + 3) / 4 : 0;
         switch (kx) {
-            case 0: run_iteration<0, FAST, NT>(S, Wt, r_first, nrows, P.sweep, c3, P.rk, acc); break;
-            case 1: run_iteration<1, FAST, NT>(S, Wt, r_first, nrows, P.sweep, c3, P.rk, acc); break;
-            case 2: run_iteration<2, FAST, NT>(S, Wt, r_first, nrows, P.sweep, c3, P.rk, acc); break;
-            default: run_iteration<3, FAST, NT>(S, Wt, r_first, nrows, P.sweep, c3, P.rk, acc); break;
+            case 0: run_iteration<0, FAST, NT>(S, Wt, wk, r_first, nrows, P.sweep, c3, P.rk, acc); break;
+            case 1: run_iteration<1, FAST, NT>(S, Wt, wk, r_first, nrows, P.sweep, c3, P.rk, acc); break;
+            case 2: run_iteration<2, FAST, NT>(S, Wt, wk, r_first, nrows, P.sweep, c3, P.rk, acc); break;
+            default: run_iteration<3, FAST, NT>(S, Wt, wk, r_first, nrows, P.sweep, c3, P.rk, acc); break;
         }
         acc_flush(acc);
         KK_PCLK(1)
@@ -700,20 +716,6 @@ __device__ __forceinline__ uint32_t res_word(int base, int w, int W, int tail) {
     return kk_smem[base + w];
 }
 
-// A thread's walk over a (rows x W) grid in steps of NT: start (a0, w0) and
-// step (da, dw), computed once per kernel so the loops issue no division.
-struct Walk {
-    int a0, w0, da, dw;
-};
-template <int NT>
-__device__ __forceinline__ Walk make_walk(int W) {
-    Walk k;
-    k.a0 = (int)threadIdx.x / W;
-    k.w0 = (int)threadIdx.x - k.a0 * W;
-    k.da = NT / W;
-    k.dw = NT - k.da * W;
-    return k;
-}
 
 template <int NT>
 __device__ __forceinline__ void res_refresh(const Tabs& S) {

@@ -12,7 +12,7 @@ torch.cuda.set_device(0)
 s = torch.cuda.current_stream()
 out = []
 for (Lx, Ly, R) in ((64, 64, 1), (256, 256, 1), (400, 400, 1), (512, 512, 1), (1024, 1024, 1),
-                    (400, 400, 37), (400, 400, 74), (400, 400, 1024)):
+                    (4096, 4096, 1), (400, 400, 37), (400, 400, 74), (400, 400, 1024)):
     L = kk.Lattice(Lx, Ly, 0.5, 0.6, 3, replicas=R, init=kk.KK_INIT_BLOCK)
     L.sweep(4, s)
     torch.cuda.synchronize()
