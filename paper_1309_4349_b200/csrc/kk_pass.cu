@@ -1254,11 +1254,24 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) cluster_kernel(const Ba
 #pragma unroll 1
     while (left > 0) {
         const int tb = (int)min64(TB, left);
-        // the block's classes (it may span two sweeps)
+        // the block's classes (it may span two sweeps, TB < 16)
         uint32_t ks[TB];
         uint32_t sw[TB];
         int js[TB];
-        {
+        int rf[TB], nr[TB];
+        Words4 sa = {}, sb = {};
+        if constexpr (L2X) {
+            // 1024-thread bands (64-register cap, ~8 items per thread): only
+            // the schedule words stay live; each iteration derives its class,
+            // sweep and light cone from them
+            sa = philox10(0u, 0u, sweep, ((uint32_t)rep << 8) | kTagSchedule, P.key0, P.key1);
+            sb = j + tb > 16 ? philox10(0u, 0u, sweep + 1u, ((uint32_t)rep << 8) | kTagSchedule, P.key0, P.key1)
+                             : sa;
+        } else {
+            // class, rows of the exact light cone of the block's remaining
+            // iterations, sweep and c3 per iteration, computed here with
+            // compile-time indices so the arrays stay in registers (a runtime
+            // index in the loop below would put them in local memory)
             uint32_t s2 = sweep;
             int j2 = j;
             Words4 sc = philox10(0u, 0u, s2, ((uint32_t)rep << 8) | kTagSchedule, P.key0, P.key1);
@@ -1273,51 +1286,81 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) cluster_kernel(const Ba
                     sc = philox10(0u, 0u, s2, ((uint32_t)rep << 8) | kTagSchedule, P.key0, P.key1);
                 }
             }
-        }
-        // per iteration of the block: class, rows of the exact light cone of
-        // the block's remaining iterations, sweep and c3 — computed here with
-        // compile-time indices so the arrays stay in registers (a runtime
-        // index in the loop below would put them in local memory)
-        int rf[TB], nr[TB];
 #pragma unroll
-        for (int t = 0; t < TB; ++t) {
-            int a = HY, bb = HY + BR;
+            for (int t = 0; t < TB; ++t) {
+                int a = HY, bb = HY + BR;
 #pragma unroll
-            for (int u = TB - 1; u > t; --u) {
-                if (u >= tb) continue;
-                const int ph = ((int)(ks[u] >> 2) + phase) & 3;
-                const int cmin = (a - 1) + ((ph - (a - 1)) & 3);
-                const int cmax = bb - ((bb - ph) & 3);
-                if (cmin <= cmax) {
-                    a = min(a, cmin - 2);
-                    bb = max(bb, cmax + 3);
+                for (int u = TB - 1; u > t; --u) {
+                    if (u >= tb) continue;
+                    const int ph = ((int)(ks[u] >> 2) + phase) & 3;
+                    const int cmin = (a - 1) + ((ph - (a - 1)) & 3);
+                    const int cmax = bb - ((bb - ph) & 3);
+                    if (cmin <= cmax) {
+                        a = min(a, cmin - 2);
+                        bb = max(bb, cmax + 3);
+                    }
                 }
+                const int r_lo = max(2, a - 1), r_hi = min(H - 2, bb + 1);
+                const int ph = ((int)(ks[t] >> 2) + phase) & 3;
+                rf[t] = r_lo + ((ph - r_lo) & 3);
+                nr[t] = r_hi > rf[t] ? (r_hi - rf[t] + 3) / 4 : 0;
             }
-            const int r_lo = max(2, a - 1), r_hi = min(H - 2, bb + 1);
-            const int ph = ((int)(ks[t] >> 2) + phase) & 3;
-            rf[t] = r_lo + ((ph - r_lo) & 3);
-            nr[t] = r_hi > rf[t] ? (r_hi - rf[t] + 3) / 4 : 0;
         }
 #pragma unroll 1
         for (int t = 0; t < tb; ++t) {
-            uint32_t kst = ks[0], swt = sw[0];
-            int jst = js[0], r_first = rf[0], nrows = nr[0];
+            uint32_t kst, swt;
+            int jst, r_first, nrows;
+            if constexpr (L2X) {
+                auto cls = [&](int jj) -> uint32_t {
+                    const int jl = jj & 15;
+                    const Words4& w4 = jj >= 16 ? sb : sa;
+                    return ((jl < 8 ? w4.a : w4.b) >> (4 * (jl & 7))) & 15u;
+                };
+                kst = cls(j + t);
+                swt = sweep + (j + t >= 16 ? 1u : 0u);
+                jst = (j + t) & 15;
+                int a = HY, bb = HY + BR;
 #pragma unroll
-            for (int u = 1; u < TB; ++u)
-                if (t == u) {
-                    kst = ks[u];
-                    swt = sw[u];
-                    jst = js[u];
-                    r_first = rf[u];
-                    nrows = nr[u];
+                for (int u = TB - 1; u > 0; --u) {
+                    if (u <= t || u >= tb) continue;
+                    const int ph = ((int)(cls(j + u) >> 2) + phase) & 3;
+                    const int cmin = (a - 1) + ((ph - (a - 1)) & 3);
+                    const int cmax = bb - ((bb - ph) & 3);
+                    if (cmin <= cmax) {
+                        a = min(a, cmin - 2);
+                        bb = max(bb, cmax + 3);
+                    }
                 }
+                const int r_lo = max(2, a - 1), r_hi = min(H - 2, bb + 1);
+                const int ph = ((int)(kst >> 2) + phase) & 3;
+                r_first = r_lo + ((ph - r_lo) & 3);
+                nrows = r_hi > r_first ? (r_hi - r_first + 3) / 4 : 0;
+            } else {
+                kst = ks[0];
+                swt = sw[0];
+                jst = js[0];
+                r_first = rf[0];
+                nrows = nr[0];
+#pragma unroll
+                for (int u = 1; u < TB; ++u)
+                    if (t == u) {
+                        kst = ks[u];
+                        swt = sw[u];
+                        jst = js[u];
+                        r_first = rf[u];
+                        nrows = nr[u];
+                    }
+            }
             const int kx = (int)(kst & 3u);
             const uint32_t c3 = ((uint32_t)rep << 8) | (uint32_t)jst;
+            // 1024-thread bands (64-register cap, ~8 items per thread): a walk
+            // recomputed per iteration keeps 4 registers free in the item loop
+            const Walk wi = L2X ? make_walk<NT>(W) : wk;
             switch (kx) {
-                case 0: band_iteration<0, NT>(S, wk, r_first, nrows, 0, 0, swt, c3, P.rk, acc); break;
-                case 1: band_iteration<1, NT>(S, wk, r_first, nrows, 0, 0, swt, c3, P.rk, acc); break;
-                case 2: band_iteration<2, NT>(S, wk, r_first, nrows, 0, 0, swt, c3, P.rk, acc); break;
-                default: band_iteration<3, NT>(S, wk, r_first, nrows, 0, 0, swt, c3, P.rk, acc); break;
+                case 0: band_iteration<0, NT>(S, wi, r_first, nrows, 0, 0, swt, c3, P.rk, acc); break;
+                case 1: band_iteration<1, NT>(S, wi, r_first, nrows, 0, 0, swt, c3, P.rk, acc); break;
+                case 2: band_iteration<2, NT>(S, wi, r_first, nrows, 0, 0, swt, c3, P.rk, acc); break;
+                default: band_iteration<3, NT>(S, wi, r_first, nrows, 0, 0, swt, c3, P.rk, acc); break;
             }
             acc_flush(acc);
             __syncthreads();
@@ -1357,9 +1400,18 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) cluster_kernel(const Ba
         if constexpr (L2X) {
             // publish side 0 = my first HY own rows, side 1 = my last HY
             uint32_t* xo = P.xch + ((int64_t)b * 2 + par) * 2 * HY * W;
-            for (int i = threadIdx.x; i < 2 * HY * W; i += NT) {
-                const int k = i / W, x = i - k * W;
-                xo[k * W + x] = kk_smem[(k < HY ? HY + k : BR + (k - HY)) * WS + kCol0 + 1 + x];
+            const Walk wx = make_walk<NT>(W);
+            {
+                int k = wx.a0, x = wx.w0;
+                for (int i = threadIdx.x; i < 2 * HY * W; i += NT) {
+                    xo[k * W + x] = kk_smem[(k < HY ? HY + k : BR + (k - HY)) * WS + kCol0 + 1 + x];
+                    k += wx.da;
+                    x += wx.dw;
+                    if (x >= W) {
+                        x -= W;
+                        ++k;
+                    }
+                }
             }
             __syncthreads();
             if (threadIdx.x == 0) {
@@ -1376,10 +1428,18 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) cluster_kernel(const Ba
             // top halo = up's last HY rows, bottom halo = dn's first HY rows
             const uint32_t* xu = P.xch + ((int64_t)up * 2 + par) * 2 * HY * W + HY * W;
             const uint32_t* xd = P.xch + ((int64_t)dn * 2 + par) * 2 * HY * W;
-            for (int i = threadIdx.x; i < 2 * HY * W; i += NT) {
-                const int k = i / W, x = i - k * W;
-                const int lr = k < HY ? k : BR + k;
-                kk_smem[lr * WS + kCol0 + 1 + x] = __ldcg((k < HY ? xu + k * W : xd + (k - HY) * W) + x);
+            {
+                int k = wx.a0, x = wx.w0;
+                for (int i = threadIdx.x; i < 2 * HY * W; i += NT) {
+                    const int lr = k < HY ? k : BR + k;
+                    kk_smem[lr * WS + kCol0 + 1 + x] = __ldcg((k < HY ? xu + k * W : xd + (k - HY) * W) + x);
+                    k += wx.da;
+                    x += wx.dw;
+                    if (x >= W) {
+                        x -= W;
+                        ++k;
+                    }
+                }
             }
             __syncthreads();
             band_refresh<NT>(S, H);

@@ -1,5 +1,5 @@
 """A/B rates of the default plan on small and mid lattices (site-updates/s),
-for comparing two builds: KK_LIB=path/to/libkk.so python tools/ab_rate.py"""
+for comparing two builds: KK_LIB=path/to/libkk.so python tools/ab_rate.py [Lx ...]"""
 import os
 import sys
 
@@ -12,7 +12,9 @@ torch.cuda.set_device(0)
 s = torch.cuda.current_stream()
 out = []
 for (Lx, Ly, R) in ((64, 64, 1), (256, 256, 1), (400, 400, 1), (512, 512, 1), (1024, 1024, 1),
-                    (4096, 4096, 1), (400, 400, 37), (400, 400, 74), (400, 400, 1024)):
+                    (4096, 4096, 1), (8192, 8192, 1), (12288, 12288, 1), (400, 400, 37), (400, 400, 74), (400, 400, 1024)):
+    if len(sys.argv) > 1 and str(Lx) not in sys.argv[1:]:
+        continue
     L = kk.Lattice(Lx, Ly, 0.5, 0.6, 3, replicas=R, init=kk.KK_INIT_BLOCK)
     L.sweep(4, s)
     torch.cuda.synchronize()
