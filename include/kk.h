@@ -98,7 +98,7 @@ typedef struct {
     int32_t halo_rows;       /* 3*T: halo rows a slab pass needs from each neighbour (R8) */
     int32_t threads;         /* CTA size of the chosen kernel */
     int32_t smem_bytes;      /* dynamic shared memory per CTA of the chosen kernel */
-    int32_t reserved;
+    int32_t pass_pdl;        /* tile kernel: 1 if consecutive passes use programmatic dependent launch */
     int64_t ctas;            /* CTAs per launch of the chosen kernel */
 } kk_plan;
 int kk_plan_config(const kk_config* cfg, int n_sm, kk_plan* out);
@@ -117,7 +117,9 @@ int kk_destroy(kk_handle h);
  * environment overrides for testing: KK_RESIDENT=0/2 (never/always when it
  * fits), KK_BAND=2 (band kernel), KK_THI/KK_TWI (tile shape),
  * KK_RES_THREADS=128/256/512, KK_PASS_THREADS=384/512, KK_TMA=0 (LDG
- * instead of TMA staging), KK_CLUSTER=2/4/8/16 (cluster kernel: the band
+ * instead of TMA staging), KK_PDL=0/1 (programmatic dependent launch of
+ * consecutive tile-kernel passes; default: when the grid fits the GPU at
+ * once), KK_CLUSTER=2/4/8/16 (cluster kernel: the band
  * kernel inside one thread-block cluster per replica, halos over DSMEM). */
 int kk_sweep(kk_handle h, int64_t n, void* stream);
 

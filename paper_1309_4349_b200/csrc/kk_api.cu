@@ -58,7 +58,7 @@ int resident_smem_bytes(const Geom& g);
 int resident_threads(const Geom& g, int64_t replicas, int nsm, int forced);
 cudaError_t launch_resident(const ResParams& P, int64_t replicas, int nt, cudaStream_t stream);
 cudaError_t launch_pass(int T, const PassParams& P, const CUtensorMap& tmap, int grid_y, int replicas,
-                        cudaStream_t stream, int threads);
+                        cudaStream_t stream, int threads, bool pdl);
 cudaError_t launch_observe(const ObsParams& P, cudaStream_t s);
 cudaError_t launch_init_block(uint32_t* lat, const Geom& g, int64_t replicas, int64_t nA, cudaStream_t s);
 cudaError_t launch_select_hist(const Geom& g, int64_t rep0, int64_t nrep, int level, const uint32_t* prefix,
@@ -109,6 +109,7 @@ struct kk_lattice {
     int resident = 0;                 // kk_sweep runs the resident kernel (whole replica in shared memory)
     int res_nt = 512;                 // its CTA size
     int pass_nt = 512;                // tile kernel CTA size (384 or 512)
+    bool pass_pdl = true;             // programmatic dependent launch of consecutive passes (KK_PDL=0: off)
     int nbands = 0;                   // > 0: kk_sweep runs the band kernel (lattice resident across all SMs)
     int cluster_size = 0;             // > 0: kk_sweep runs the cluster kernel (one cluster per replica)
     int cluster_tb = 1;               // its iterations per halo exchange (1: band_kernel<256, true>)
@@ -328,7 +329,7 @@ int run_pass(kk_lattice* h, int region, const uint32_t* ht, const uint32_t* hb, 
     } else {
         return fail(KK_ERR_ARG, "kk_pass: bad region");
     }
-    KK_CUDA(launch_pass(h->T, P, h->tmap[h->cur], grid_y, (int)h->R, s, h->pass_nt));  // grid.z = replica (R <= 65535)
+    KK_CUDA(launch_pass(h->T, P, h->tmap[h->cur], grid_y, (int)h->R, s, h->pass_nt, h->pass_pdl));  // grid.z = replica (R <= 65535)
     return KK_OK;
 }
 
@@ -543,6 +544,14 @@ int plan_handle(kk_lattice* h, const kk_config* c, int T, int nsm) {
         const int forced = env_int("KK_PASS_THREADS", 0);
         const int64_t ctas = (int64_t)h->tiles_x * h->bands * h->R;
         h->pass_nt = (forced == 384 || forced == 512) ? forced : (ctas > 4 * (int64_t)nsm ? 384 : 512);
+        // Programmatic dependent launch of consecutive passes: the next
+        // pass's CTAs start (launch + tables) while this one drains.  It
+        // pays on grids that fit the GPU at once (2 CTAs per SM): 1024^2
+        // 32.0 -> 39.2, 2048^2 102 -> 118, 4096^2 214 -> 230 G/s; on
+        // many-wave grids the early CTAs idle in slots (16384^2 412 -> 397,
+        // 65536^2 neutral), so it is off there (tools/pdl_rate.py).
+        const int pdl = env_int("KK_PDL", -1);
+        h->pass_pdl = pdl < 0 ? ctas <= 2 * (int64_t)nsm : pdl != 0;
     }
     const int mode = env_int("KK_RESIDENT", 1);
     const int64_t tile_ctas = (int64_t)h->tiles_x * h->bands;
@@ -656,6 +665,7 @@ int kk_plan_config(const kk_config* c, int n_sm, kk_plan* out) {
     out->halo_rows = tmp.hy;
     if (out->kernel == KK_KERNEL_TILE) {
         out->threads = tmp.pass_nt;
+        out->pass_pdl = tmp.pass_pdl ? 1 : 0;
         out->smem_bytes = pass_smem_bytes(T, tmp.THI, tmp.TWI);
         out->ctas = (int64_t)tmp.tiles_x * tmp.bands * tmp.R;
     } else if (out->kernel == KK_KERNEL_RESIDENT) {

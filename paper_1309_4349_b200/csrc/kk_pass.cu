@@ -156,6 +156,10 @@ extern __shared__ __align__(128) uint32_t kk_smem[];
 // starts at the beginning of the CTA's shared window, which keeps the tile
 // 128-byte aligned for the TMA destination.
 
+// ---- programmatic dependent launch (no-ops when the grid was launched without it)
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---- TMA (cp.async.bulk.tensor) staging of interior tiles ----------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -515,7 +519,14 @@ __global__ void __launch_bounds__(NT, kMinBlocks)
     const int64_t gw0 = X0 / 32 - 1;
     const bool tma_tile = P.use_tma && Y0 - HY >= 0 && Y0 - HY + H <= g.rows && gw0 - kCol0 >= 0 &&
                           gw0 - kCol0 + WS <= g.W;
+    // Programmatic dependent launch: this grid may start while the previous
+    // pass is still running (kk_pass launches it with programmatic stream
+    // serialization), so nothing below may touch global memory before
+    // griddepcontrol.wait.  Thread 0 waits first and issues the TMA boxes;
+    // the other threads build the per-pass tables (kernel parameters only)
+    // meanwhile and wait before the LDG staging.
     if (tma_tile && threadIdx.x == 0) {
+        grid_dep_wait();
         mbar_init(tma_bar, 1);
         const int nbox = (H + P.box_h - 1) / P.box_h;
         mbar_expect_tx(tma_bar, (uint32_t)(nbox * P.box_h * WS * 4));
@@ -551,6 +562,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks)
     // ---- stage tile + halo, part 2: wait for the TMA boxes (the barrier
     // makes thread 0's mbarrier init visible first), or copy with LDG
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    grid_dep_wait();  // the previous pass's writes (dst = our src) and its reads of our dst are done
     if (tma_tile) {
         __syncthreads();
         mbar_wait(tma_bar, 0);
@@ -588,6 +600,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks)
         }
     }
     __syncthreads();
+    grid_dep_launch();  // the next pass may be scheduled onto SMs this grid frees
     KK_PCLK(0)
 
     const Words4 sched = philox10(0u, 0u, P.sweep, ((uint32_t)rep << 8) | kTagSchedule, P.key0, P.key1);
@@ -1767,21 +1780,36 @@ cudaError_t launch_band_tb(const BandParams& P, int TB, cudaStream_t stream) {
 }
 
 cudaError_t launch_pass(int T, const PassParams& P, const CUtensorMap& tmap, int grid_y, int replicas,
-                        cudaStream_t stream, int threads) {
+                        cudaStream_t stream, int threads, bool pdl) {
     const int smem = pass_smem_bytes(T, P.THI, P.TWI);
     dim3 grid(P.tiles_x, grid_y, replicas);
     if (grid_y == 0) return cudaSuccess;
     cudaError_t e = cudaSuccess;
+    // Programmatic stream serialization: the grid may launch once every CTA
+    // of the preceding kernel has passed griddepcontrol.launch_dependents (or
+    // exited); its own griddepcontrol.wait orders it after that kernel's
+    // completion, so only the launch and the table setup overlap.
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.dynamicSmemBytes = (size_t)smem;
+    cfg.stream = stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
 #define KK_LAUNCH_NT(TT, NTT)                                                                   \
+    cfg.blockDim = dim3(NTT);                                                                   \
     if (P.g.tail == 0) {                                                                        \
         e = ensure_dynamic_smem((const void*)pass_kernel<TT, true, NTT>, smem);                 \
         if (e != cudaSuccess) return e;                                                         \
-        pass_kernel<TT, true, NTT><<<grid, NTT, smem, stream>>>(tmap, P);                       \
+        e = cudaLaunchKernelEx(&cfg, pass_kernel<TT, true, NTT>, tmap, P);                      \
     } else {                                                                                    \
         e = ensure_dynamic_smem((const void*)pass_kernel<TT, false, NTT>, smem);                \
         if (e != cudaSuccess) return e;                                                         \
-        pass_kernel<TT, false, NTT><<<grid, NTT, smem, stream>>>(tmap, P);                      \
-    }
+        e = cudaLaunchKernelEx(&cfg, pass_kernel<TT, false, NTT>, tmap, P);                     \
+    }                                                                                           \
+    if (e != cudaSuccess) return e;
 #define KK_LAUNCH(TT)                                                                           \
     case TT:                                                                                    \
         if (threads == 384) {                                                                   \

@@ -307,6 +307,23 @@ def test_tile_kernel_tma_staging_with_replicas(tma):
     _run_parity(2048, 256, 0.5, 0.7, 2048 + tma, 3, R=3, env={"KK_TMA": tma})
 
 
+@pytest.mark.parametrize("pdl,Lx,Ly,env", [
+    (1, 2048, 256, {}), (0, 2048, 256, {}),
+    (1, 1000, 44, {"KK_TWI": 5, "KK_THI": 12}),    # Lx % 32 != 0: LDG staging, ragged tiles
+])
+def test_tile_kernel_programmatic_dependent_launch(pdl, Lx, Ly, env, monkeypatch):
+    """Consecutive passes launched with programmatic stream serialization
+    (the next pass's CTAs start before the previous pass ends and wait in
+    griddepcontrol.wait before touching the lattice) against the oracle over
+    several sweeps, forced on and off regardless of the grid size."""
+    from paper_1309_4349_b200 import kk
+    for key, v in {**env, "KK_PDL": pdl, "KK_RESIDENT": 0, "KK_CLUSTER": 0, "KK_BAND": 0}.items():
+        monkeypatch.setenv(key, str(v))
+    p = kk.plan(Lx, Ly, replicas=2)
+    assert p["kernel"] == "tile" and p["pass_pdl"] == pdl
+    _run_parity(Lx, Ly, 0.5, 0.7, Lx + 17 * pdl, 4, R=2)
+
+
 def test_cluster_histogram_total_over_replicas():
     """The replica-summed histogram equals the sum of the oracle's per-replica
     histograms (BASELINE configs[3]-style ensemble statistics)."""

@@ -33,11 +33,13 @@ def test_bench_lattice_plan():
     assert p["smem_bytes"] <= SMEM_2_PER_SM          # two CTAs per SM
     assert p["ctas"] == p["tiles_x"] * p["bands"] >= 148 * 20
     assert p["threads"] == 384                      # many waves: 80-register CTAs
+    assert p["pass_pdl"] == 0                       # early CTAs would idle in slots
 
 
 def test_mid_size_lattice_fills_every_sm():
     p = kk.plan(4096, 4096)
     assert p["kernel"] == "tile" and p["ctas"] >= 148 and p["threads"] == 512
+    assert p["pass_pdl"] == 1                       # one wave: next pass launches under this one
     q = kk.plan(8192, 8192)                      # band kernel: one band per SM, L2 halos every 4 iterations
     assert q["kernel"] == "band" and q["ctas"] == 148 and q["threads"] == 1024
     assert kk.plan(16384, 16384)["kernel"] == "tile"   # bands no longer fit in shared memory
