@@ -585,17 +585,22 @@ int plan_handle(kk_lattice* h, const kk_config* c, int T, int nsm) {
     // replicas' clusters fit on the GPU at once (400^2: 1 replica 1.9 -> 5.4
     // G/s with 8 CTAs, 37 replicas 69 -> 107 with 4, 74 replicas 138 -> 206
     // with 2; 256^2: 2.0 -> 3.1; tools/cluster_rate.py, cluster_c2.py).
-    // KK_CLUSTER=0 never, =2/4/8/16 forces.
+    // Up to 4 replicas of >= 320 rows take 16-CTA (non-portable) clusters:
+    // 400^2 6.6 -> 7.4 G/s, 512^2 9.9 -> 13.0, 4 x 400^2 26.5 -> 29.5; at 8
+    // replicas (128 SMs) 8-CTA clusters win again, 52.8 vs 45.1
+    // (tools/cluster16.py).  KK_CLUSTER=0 never, =2/4/8/16 forces.
     const int cmode = env_int("KK_CLUSTER", -1);
     int csize = cmode;
     if (cmode < 0) {
         csize = 0;
         if (h->resident && h->g.rows >= 192 && h->g.Lx >= 192)
-            for (int c : {8, 4, 2})
-                if (h->R * c <= nsm) {
+            for (int c : {16, 8, 4, 2}) {
+                if (c == 16 && (h->g.rows < 320 || h->R * 32 > nsm)) continue;
+                if (h->R * c <= nsm && h->g.periodic && cluster_smem_bytes(h->g, c) > 0) {
                     csize = c;
                     break;
                 }
+            }
     }
     h->cluster_size = (csize > 0 && h->g.periodic && cluster_smem_bytes(h->g, csize) > 0) ? csize : 0;
     {

@@ -47,8 +47,11 @@ def test_mid_size_lattice_fills_every_sm():
 
 def test_small_and_replica_batches_are_resident():
     assert kk.plan(64, 64)["kernel"] == "resident"
-    assert kk.plan(400, 400)["kernel"] == "cluster"              # the paper's lattice: one 8-CTA cluster
-    assert kk.plan(400, 400)["ctas"] == 8
+    assert kk.plan(400, 400)["kernel"] == "cluster"              # the paper's lattice: one 16-CTA cluster
+    assert kk.plan(400, 400)["ctas"] == 16
+    assert kk.plan(400, 400, replicas=4)["ctas"] == 4 * 16      # up to 4 replicas: 16-CTA clusters
+    assert kk.plan(400, 400, replicas=5)["ctas"] == 5 * 8
+    assert kk.plan(256, 256)["ctas"] == 8                        # < 320 rows: 8-CTA clusters
     assert kk.plan(400, 400, replicas=16)["ctas"] == 16 * 8     # 16 clusters of 8 CTAs fit on 148 SMs
     assert kk.plan(400, 400, replicas=37)["ctas"] == 37 * 4     # then clusters of 4, of 2
     assert kk.plan(400, 400, replicas=74)["ctas"] == 74 * 2
@@ -110,7 +113,7 @@ def test_plan_invariants(Lx, Ly, R, T):
     elif p["kernel"] == "resident":
         assert p["ctas"] == R and Lx >= 64 and p["threads"] in (128, 256, 512)
     elif p["kernel"] == "cluster":
-        assert p["ctas"] % R == 0 and p["ctas"] // R in (2, 4, 8) and p["ctas"] <= 148 and Ly >= 192
+        assert p["ctas"] % R == 0 and p["ctas"] // R in (2, 4, 8, 16) and p["ctas"] <= 148 and Ly >= 192
 
 
 def test_invalid_configs_fail_without_a_gpu():

@@ -41,6 +41,10 @@ def main():
         # 18 such handles oversubscribe the SMs; one SM per replica (resident
         # kernel) is the better split for many concurrent handles
         os.environ["KK_CLUSTER"] = "0"
+    if a.seeds == 1 and "KK_CLUSTER" not in os.environ:
+        # one lattice per handle would take a 16-CTA cluster; 18 concurrent
+        # handles fit the GPU at once with 8-CTA clusters (144 SMs)
+        os.environ["KK_CLUSTER"] = "8"
     omegas = [0.2, 0.3, 0.4, 0.5, 0.6, 0.7, 0.8, 0.9, 1.0]
     fracs = [0.5, 0.3]
     pts = [(f, om) for f in fracs for om in omegas]
