@@ -543,7 +543,13 @@ int plan_handle(kk_lattice* h, const kk_config* c, int T, int nsm) {
     {
         const int forced = env_int("KK_PASS_THREADS", 0);
         const int64_t ctas = (int64_t)h->tiles_x * h->bands * h->R;
-        h->pass_nt = (forced == 384 || forced == 512) ? forced : (ctas > 4 * (int64_t)nsm ? 384 : 512);
+        // Few-wave grids whose widest iteration (interior + light cone, T = 8)
+        // fits one round of 384 items take 384 threads too: 1024^2 39.2 ->
+        // 40.4, 1536^2 79.3 -> 82.2, 2048^2 117.8 -> 121.4 G/s; from 2560^2
+        // (92 x 16 tiles, ~520 items) 512 wins (tools/nt_compare.py).
+        const bool one_round = (int64_t)(h->THI / 4 + 6) * (h->TWI + 2) <= 384;
+        h->pass_nt = (forced == 384 || forced == 512) ? forced
+                     : ((ctas > 4 * (int64_t)nsm || one_round) ? 384 : 512);
         // Programmatic dependent launch of consecutive passes: the next
         // pass's CTAs start (launch + tables) while this one drains.  It
         // pays on grids that fit the GPU at once (2 CTAs per SM): 1024^2

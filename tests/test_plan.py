@@ -40,6 +40,8 @@ def test_mid_size_lattice_fills_every_sm():
     p = kk.plan(4096, 4096)
     assert p["kernel"] == "tile" and p["ctas"] >= 148 and p["threads"] == 512
     assert p["pass_pdl"] == 1                       # one wave: next pass launches under this one
+    r = kk.plan(2048, 2048)                         # one wave, every iteration one round of 384 items
+    assert r["kernel"] == "tile" and r["ctas"] <= 296 and r["threads"] == 384 and r["pass_pdl"] == 1
     q = kk.plan(8192, 8192)                      # band kernel: one band per SM, L2 halos every 4 iterations
     assert q["kernel"] == "band" and q["ctas"] == 148 and q["threads"] == 1024
     assert kk.plan(16384, 16384)["kernel"] == "tile"   # bands no longer fit in shared memory
