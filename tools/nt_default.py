@@ -1,5 +1,5 @@
-"""Tile-kernel CTA size (KK_PASS_THREADS) across lattice sizes.
-Usage: python tools/nt_compare.py [sizes...]"""
+"""Default plan vs forced CTA sizes on one-wave tile grids.
+Usage: python tools/nt_default.py [sizes...]"""
 import os
 import sys
 
@@ -10,11 +10,10 @@ from paper_1309_4349_b200 import kk  # noqa: E402
 
 torch.cuda.set_device(0)
 s = torch.cuda.current_stream()
-sizes = [int(a) for a in sys.argv[1:]] or [2048, 4096, 8192, 16384, 32768, 65536]
-for L_ in sizes:
-    line = f"{L_}^2:"
-    for nt in [int(v) for v in os.environ.get("NTS", "384,512").split(",")]:
-        os.environ["KK_PASS_THREADS"] = str(nt)
+for L_ in [int(a) for a in sys.argv[1:]] or (5120, 6144, 7168):
+    line = f"{L_}^2 (default {kk.plan(L_, L_)['threads']}):"
+    for nt in ("0", "512", "1024"):
+        os.environ["KK_PASS_THREADS"] = nt
         L = kk.Lattice(L_, L_, 0.5, 0.6, 3, init=kk.KK_INIT_BLOCK)
         L.sweep(1, s)
         torch.cuda.synchronize()
@@ -24,6 +23,6 @@ for L_ in sizes:
         L.sweep(n, s)
         e1.record(s)
         torch.cuda.synchronize()
-        line += f" {nt}: {n * L_ * L_ / e0.elapsed_time(e1) / 1e6:.1f}"
+        line += f" {'default' if nt == '0' else nt}: {n * L_ * L_ / e0.elapsed_time(e1) / 1e6:.1f}"
         L.close()
     print(line + " G/s", flush=True)
