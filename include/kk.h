@@ -116,7 +116,7 @@ int kk_destroy(kk_handle h);
  * larger lattices the tile kernel (16/T launches per sweep);
  * environment overrides for testing: KK_RESIDENT=0/2 (never/always when it
  * fits), KK_BAND=2 (band kernel), KK_THI/KK_TWI (tile shape),
- * KK_RES_THREADS=128/256/512, KK_PASS_THREADS=384/512/1024 (1024: T = 8), KK_TMA=0 (LDG
+ * KK_RES_THREADS=128/256/512, KK_PASS_THREADS=384/512/640 (640: T = 8), KK_TMA=0 (LDG
  * instead of TMA staging), KK_PDL=0/1 (programmatic dependent launch of
  * consecutive tile-kernel passes; default: when the grid fits the GPU at
  * once), KK_CLUSTER=2/4/8/16 (cluster kernel: the band

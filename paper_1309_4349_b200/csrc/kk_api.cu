@@ -539,23 +539,23 @@ int plan_handle(kk_lattice* h, const kk_config* c, int T, int nsm) {
     // tools/single_small.py); 2 = whenever the replica fits; 0 = never.
     // tile kernel CTA size: 384 threads get 80 registers (vs 64 at 512) and
     // ~4% shorter items (no rematerialised addresses), which wins when there
-    // are many waves of tiles; few-wave grids keep 512 (more warps per tile).
+    // are many waves of tiles.
     {
         const int forced = env_int("KK_PASS_THREADS", 0);
         const int64_t ctas = (int64_t)h->tiles_x * h->bands * h->R;
         // Few-wave grids whose widest iteration (interior + light cone, T = 8)
         // fits one round of 384 items take 384 threads too: 1024^2 39.2 ->
-        // 40.4, 1536^2 79.3 -> 82.2, 2048^2 117.8 -> 121.4 G/s; from 2560^2
-        // (92 x 16 tiles, ~520 items) 512 wins (tools/nt_compare.py).
-        // One-wave grids with >= 1536 items in the widest iteration (5120^2:
-        // 180 x 32 tiles) take 1024 threads: two rounds instead of four and
-        // twice the warps, 250 -> 265 G/s; at 4096^2 (~1150 items) 512 and
-        // 1024 tie, at 16384^2 (many waves) 1024 loses 7%.
+        // 40.4, 1536^2 79.3 -> 82.2, 2048^2 117.8 -> 121.4 G/s
+        // (tools/nt_compare.py).  Other one-wave grids take 640 threads (one CTA per SM, up to 96
+        // registers): 20 warps and about two rounds per iteration instead of
+        // two-and-a-bit — 2560^2 149 -> 159, 4096^2 231 -> 247, 5120^2 253 ->
+        // 271, 6144^2 290 -> 314 G/s; 576/768/1024 were within 2% or worse
+        // (tools/nt_compare.py, profiles/r01_nt_wide.txt).
         const int64_t items = (int64_t)(h->THI / 4 + 6) * (h->TWI + 2);
         const bool one_round = items <= 384;
-        const bool wide = T == 8 && ctas <= nsm && items >= 1536;
-        h->pass_nt = (forced == 384 || forced == 512 || (forced == 1024 && T == 8)) ? forced
-                     : ((ctas > 4 * (int64_t)nsm || one_round) ? 384 : (wide ? 1024 : 512));
+        const bool wide = T == 8 && ctas <= nsm && !one_round;
+        h->pass_nt = (forced == 384 || forced == 512 || (forced == 640 && T == 8)) ? forced
+                     : ((ctas > 4 * (int64_t)nsm || one_round) ? 384 : (wide ? 640 : 512));
         // Programmatic dependent launch of consecutive passes: the next
         // pass's CTAs start (launch + tables) while this one drains.  It
         // pays on grids that fit the GPU at once (2 CTAs per SM): 1024^2

@@ -480,7 +480,7 @@ __device__ unsigned long long kk_pass_clk[16];
 #define KK_PCLK(k)
 #endif
 template <int T, bool FAST, int NT>
-__global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : kMinBlocks)
+__global__ void __launch_bounds__(NT, NT > 512 ? 1 : kMinBlocks)
     pass_kernel(const __grid_constant__ CUtensorMap tmap, const PassParams P) {
 #ifdef KK_PASS_CLK
     long long c0clk = clock64();
@@ -1814,8 +1814,8 @@ cudaError_t launch_pass(int T, const PassParams& P, const CUtensorMap& tmap, int
     case TT:                                                                                    \
         if (threads == 384) {                                                                   \
             KK_LAUNCH_NT(TT, 384)                                                               \
-        } else if (TT == 8 && threads == 1024) {                                                \
-            KK_LAUNCH_NT(8, 1024)                                                               \
+        } else if (TT == 8 && threads == 640) {                                                 \
+            KK_LAUNCH_NT(8, 640)                                                                \
         } else {                                                                                \
             KK_LAUNCH_NT(TT, 512)                                                               \
         }                                                                                       \

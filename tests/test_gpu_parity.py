@@ -324,12 +324,12 @@ def test_tile_kernel_programmatic_dependent_launch(pdl, Lx, Ly, env, monkeypatch
     _run_parity(Lx, Ly, 0.5, 0.7, Lx + 17 * pdl, 4, R=2)
 
 
-def test_tile_kernel_1024_threads_default_5120():
-    """5120^2 is a one-wave grid of 180 x 32 tiles: the plan takes 1024-thread
-    CTAs (two rounds of items per iteration); one full sweep against the oracle."""
+def test_tile_kernel_640_threads_default_5120():
+    """5120^2 is a one-wave grid of 180 x 32 tiles: the plan takes 640-thread
+    CTAs (one per SM, up to 96 registers); one full sweep against the oracle."""
     from paper_1309_4349_b200 import kk
     p = kk.plan(5120, 5120)
-    assert p["kernel"] == "tile" and p["threads"] == 1024
+    assert p["kernel"] == "tile" and p["threads"] == 640
     _run_parity(5120, 5120, 0.5, 0.6, 5120, 1)
 
 
@@ -337,13 +337,13 @@ def test_tile_kernel_1024_threads_default_5120():
     (2048, 256, {}),
     (1000, 44, {"KK_TWI": 5, "KK_THI": 12}),    # Lx % 32 != 0: per-centre draw path, LDG staging
 ])
-def test_tile_kernel_1024_threads_forced(Lx, Ly, env, monkeypatch):
-    """KK_PASS_THREADS=1024 on small and ragged shapes with replicas."""
+def test_tile_kernel_640_threads_forced(Lx, Ly, env, monkeypatch):
+    """KK_PASS_THREADS=640 on small and ragged shapes with replicas."""
     from paper_1309_4349_b200 import kk
-    for key, v in {**env, "KK_PASS_THREADS": 1024, "KK_RESIDENT": 0, "KK_CLUSTER": 0, "KK_BAND": 0}.items():
+    for key, v in {**env, "KK_PASS_THREADS": 640, "KK_RESIDENT": 0, "KK_CLUSTER": 0, "KK_BAND": 0}.items():
         monkeypatch.setenv(key, str(v))
     p = kk.plan(Lx, Ly, replicas=2)
-    assert p["kernel"] == "tile" and p["threads"] == 1024
+    assert p["kernel"] == "tile" and p["threads"] == 640
     _run_parity(Lx, Ly, 0.5, 0.7, Lx + 3, 3, R=2)
 
 

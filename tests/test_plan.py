@@ -38,9 +38,10 @@ def test_bench_lattice_plan():
 
 def test_mid_size_lattice_fills_every_sm():
     p = kk.plan(4096, 4096)
-    assert p["kernel"] == "tile" and p["ctas"] >= 148 and p["threads"] == 512
+    assert p["kernel"] == "tile" and p["ctas"] >= 148
     assert p["pass_pdl"] == 1                       # one wave: next pass launches under this one
-    assert kk.plan(5120, 5120)["threads"] == 1024   # one wave, >= 1536 items per iteration
+    assert kk.plan(5120, 5120)["threads"] == 640    # one wave, > 384 items per iteration
+    assert p["threads"] == 640                      # 4096^2 likewise
     r = kk.plan(2048, 2048)                         # one wave, every iteration one round of 384 items
     assert r["kernel"] == "tile" and r["ctas"] <= 296 and r["threads"] == 384 and r["pass_pdl"] == 1
     q = kk.plan(8192, 8192)                      # band kernel: one band per SM, L2 halos every 4 iterations

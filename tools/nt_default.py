@@ -10,9 +10,9 @@ from paper_1309_4349_b200 import kk  # noqa: E402
 
 torch.cuda.set_device(0)
 s = torch.cuda.current_stream()
-for L_ in [int(a) for a in sys.argv[1:]] or (5120, 6144, 7168):
+for L_ in [int(a) for a in sys.argv[1:]] or (2560, 3072, 4096, 5120, 6144, 7168):
     line = f"{L_}^2 (default {kk.plan(L_, L_)['threads']}):"
-    for nt in ("0", "512", "1024"):
+    for nt in ("0", "512", "640"):
         os.environ["KK_PASS_THREADS"] = nt
         L = kk.Lattice(L_, L_, 0.5, 0.6, 3, init=kk.KK_INIT_BLOCK)
         L.sweep(1, s)
