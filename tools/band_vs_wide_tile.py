@@ -1,5 +1,5 @@
 """Band kernel (default 8192^2..12288^2) vs a one-wave tile grid with
-1024-thread CTAs and PDL.  Usage: python tools/band_vs_wide_tile.py"""
+640-thread CTAs and PDL.  Usage: python tools/band_vs_wide_tile.py"""
 import os
 import sys
 
@@ -37,7 +37,7 @@ def rate(L_, env):
 
 for L_, thi, twi in ((8192, 224, 64), (8192, 112, 128), (10240, 356, 64), (12288, 512, 64), (12288, 256, 128)):
     line = f"{L_}^2: default {rate(L_, {}):.1f}"
-    for nt in ("1024", "512"):
+    for nt in ("640", "512"):
         line += (f" tile {thi}x{twi} nt={nt} pdl=1: "
                  f"{rate(L_, {'KK_BAND': '0', 'KK_THI': str(thi), 'KK_TWI': str(twi), 'KK_PASS_THREADS': nt, 'KK_PDL': '1'}):.1f}")
     print(line + " G/s", flush=True)
