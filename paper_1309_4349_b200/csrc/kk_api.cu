@@ -108,7 +108,8 @@ struct kk_lattice {
     int use_tma = 0, box_h = 0;
     int resident = 0;                 // kk_sweep runs the resident kernel (whole replica in shared memory)
     int res_nt = 512;                 // its CTA size
-    int pass_nt = 512;                // tile kernel CTA size (384 or 512)
+    int pass_nt = 512;                // tile kernel CTA size (384, 512 or 640)
+    bool tall = false;                // tile kernel: one tall tile per SM at a time (640 threads)
     bool pass_pdl = true;             // programmatic dependent launch of consecutive passes (KK_PDL=0: off)
     int nbands = 0;                   // > 0: kk_sweep runs the band kernel (lattice resident across all SMs)
     int cluster_size = 0;             // > 0: kk_sweep runs the cluster kernel (one cluster per replica)
@@ -244,6 +245,24 @@ void choose_tiles(kk_lattice* h, int nsm) {
                     bt = twi_t;
                     bh = h->THI;
                 }
+            }
+        }
+        // Many-wave grids (>= 16 two-per-SM CTAs per SM): one tall tile per SM
+        // at a time (64 words x <= 600 rows, the fewest bands, 640 threads,
+        // up to 227 KB) halves the light-cone share of the items: 65536^2 483
+        // -> 490 G/s (64 x 596; 560 rows 486, 660 rows 489); 16384^2 has too
+        // few waves (1.5% slower), tools/tall_tiles.py.
+        const bool many_waves = [&] {
+            set_tiles(h, bt, bh);
+            return (int64_t)h->tiles_x * h->bands * h->R >= 16 * (int64_t)2 * nsm;
+        }();
+        h->tall = false;
+        if (T == 8 && many_waves && env_int("KK_TALL", 1)) {
+            set_tiles(h, 64, 600);
+            if (h->TWI == 64 && pass_smem_bytes(T, h->THI, h->TWI) <= 227 * 1024) {
+                bt = 64;
+                bh = h->THI;
+                h->tall = true;
             }
         }
         set_tiles(h, bt, bh);
@@ -555,7 +574,8 @@ int plan_handle(kk_lattice* h, const kk_config* c, int T, int nsm) {
         const bool one_round = items <= 384;
         const bool wide = T == 8 && ctas <= nsm && !one_round;
         h->pass_nt = (forced == 384 || forced == 512 || (forced == 640 && T == 8)) ? forced
-                     : ((ctas > 4 * (int64_t)nsm || one_round) ? 384 : (wide ? 640 : 512));
+                     : (h->tall || wide) ? 640
+                     : ((ctas > 4 * (int64_t)nsm || one_round) ? 384 : 512);
         // Programmatic dependent launch of consecutive passes: the next
         // pass's CTAs start (launch + tables) while this one drains.  It
         // pays on grids that fit the GPU at once (2 CTAs per SM): 1024^2

@@ -26,14 +26,20 @@ def _lib():
             os.environ[k] = v
 
 
-def test_bench_lattice_plan():
+def test_bench_lattice_plan(monkeypatch):
     p = kk.plan(65536, 65536)
     assert p["kernel"] == "tile" and p["iters_per_pass"] == 8 and p["halo_rows"] == 24
-    assert p["tile_words"] == 64 and 300 <= p["tile_rows"] <= 340
-    assert p["smem_bytes"] <= SMEM_2_PER_SM          # two CTAs per SM
+    assert p["tile_words"] == 64 and 540 <= p["tile_rows"] <= 600   # tall tiles, one per SM at a time
+    assert SMEM_2_PER_SM < p["smem_bytes"] <= 227 * 1024
     assert p["ctas"] == p["tiles_x"] * p["bands"] >= 148 * 20
-    assert p["threads"] == 384                      # many waves: 80-register CTAs
+    assert p["threads"] == 640
     assert p["pass_pdl"] == 0                       # early CTAs would idle in slots
+    monkeypatch.setenv("KK_TALL", "0")              # two CTAs per SM: the cost-model tiles
+    q = kk.plan(65536, 65536)
+    monkeypatch.delenv("KK_TALL")
+    assert q["tile_words"] == 64 and 300 <= q["tile_rows"] <= 340 and q["smem_bytes"] <= SMEM_2_PER_SM
+    assert q["threads"] == 384                      # many waves: 80-register CTAs
+    assert kk.plan(16384, 16384)["threads"] == 512  # too few waves for tall tiles
 
 
 def test_mid_size_lattice_fills_every_sm():
@@ -113,7 +119,7 @@ def test_plan_invariants(Lx, Ly, R, T):
     assert p["halo_rows"] == 3 * (T or 8)
     if p["kernel"] == "tile":
         assert p["ctas"] == p["tiles_x"] * p["bands"] * R
-        assert p["smem_bytes"] <= SMEM_2_PER_SM or os.environ.get("KK_THI")
+        assert p["smem_bytes"] <= SMEM_2_PER_SM or os.environ.get("KK_THI") or p["threads"] == 640
     elif p["kernel"] == "resident":
         assert p["ctas"] == R and Lx >= 64 and p["threads"] in (128, 256, 512)
     elif p["kernel"] == "cluster":

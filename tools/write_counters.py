@@ -1,0 +1,40 @@
+"""Write profiles/pass_kernel_counters.json (read by bench.py for the roofline)
+from an ncu --set full capture of one bench-lattice pass.
+Usage: python tools/write_counters.py report.ncu-rep updates_per_launch "tile description" [out.json]"""
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+rep, upd, tile = sys.argv[1], float(sys.argv[2]), sys.argv[3]
+out = sys.argv[4] if len(sys.argv) > 4 else os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                                         "profiles", "pass_kernel_counters.json")
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(raw)))
+h, units, v = rows[0], rows[1], rows[2]
+
+
+def val(name):
+    x = float(v[h.index(name)].replace(",", ""))
+    u = units[h.index(name)]
+    return x * {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1e-3, "msecond": 1.0, "nsecond": 1e-6}.get(u, 1.0)
+
+
+name = v[h.index("Kernel Name")]
+d = {
+    "kernel": name.split("(")[0].replace("void ", "").replace("unnamed>::", ""),
+    "T": 8,
+    "thread_inst_per_update": val("thread_inst_executed") / upd,
+    "dram_bytes_per_update": (val("dram__bytes_read.sum") + val("dram__bytes_write.sum")) / upd,
+    "launch_ms_ncu": val("gpu__time_duration.sum"),
+    "issue_active_pct": round(val("smsp__issue_active.avg.pct_of_peak_sustained_active"), 2),
+    "alu_pipe_pct": round(val("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"), 2),
+    "fma_pipe_pct": round(val("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"), 2),
+    "source": f"ncu --set full --clock-control none, tools/profile_pass.py 65536 65536 1 8 (bench lattice); {os.path.basename(rep)}",
+    "tile": tile,
+}
+with open(out, "w") as f:
+    json.dump(d, f, indent=1)
+print(json.dumps(d, indent=1))
