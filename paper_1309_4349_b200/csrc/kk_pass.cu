@@ -13,6 +13,9 @@
 //    interior is exact; the rows actually processed follow the exact light
 //    cone of the pass's classes).  The lattice crosses HBM once per T
 //    iterations (read tile+halo, write the interior to the other buffer).
+//    CTA sizes 384/512/640 (640: one tall tile per SM on the largest grids,
+//    or one tile per SM on one-wave grids); on one-wave grids consecutive
+//    passes are chained by programmatic dependent launch (griddepcontrol).
 //  * resident_kernel<NT>: replicas that fit in one SM's shared memory; one
 //    CTA per replica runs every iteration of a kk_sweep call in place, the
 //    periodic wrap kept as rebuilt copies.
