@@ -88,10 +88,11 @@ int kk_create_ex(kk_handle* out, const kk_config* cfg);
  * (<= 0: query cfg->device or the current device).  The plan never changes
  * results (every kernel is bit-identical); it decides speed.
  * Honours the same environment overrides as kk_create_ex (kk_sweep). */
-enum { KK_KERNEL_TILE = 0, KK_KERNEL_RESIDENT = 1, KK_KERNEL_BAND = 2, KK_KERNEL_CLUSTER = 3 };
+enum { KK_KERNEL_TILE = 0, KK_KERNEL_RESIDENT = 1, KK_KERNEL_BAND = 2, KK_KERNEL_CLUSTER = 3,
+       KK_KERNEL_PLANAR = 4 /* tile passes on the plane-interleaved layout (Lx % 128 == 0) */ };
 typedef struct {
     int32_t kernel;          /* KK_KERNEL_*: what kk_sweep launches */
-    int32_t iters_per_pass;  /* T of the tile kernel (kk_pass always uses the tile kernel) */
+    int32_t iters_per_pass;  /* T of the tile kernel (kk_pass always uses a tile kernel: planar if Lx % 128 == 0) */
     int32_t tile_rows;       /* tile kernel: interior rows per CTA (THI, multiple of 4) */
     int32_t tile_words;      /* tile kernel: interior 32-bit words per CTA row (TWI) */
     int32_t tiles_x, bands;  /* tile kernel: tiles per row, row bands per replica */
@@ -100,6 +101,8 @@ typedef struct {
     int32_t smem_bytes;      /* dynamic shared memory per CTA of the chosen kernel */
     int32_t pass_pdl;        /* tile kernel: 1 if consecutive passes use programmatic dependent launch */
     int64_t ctas;            /* CTAs per launch of the chosen kernel */
+    int32_t tma_boxes;       /* tile kernels: cp.async.bulk.tensor boxes per interior tile (0: LDG staging) */
+    int32_t reserved;
 } kk_plan;
 int kk_plan_config(const kk_config* cfg, int n_sm, kk_plan* out);
 

@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libkk.so")
-SOURCES = ["kk_api.cu", "kk_pass.cu", "kk_observe.cu", "kk_ccl.cu"]
+SOURCES = ["kk_api.cu", "kk_pass.cu", "kk_planar.cu", "kk_observe.cu", "kk_ccl.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

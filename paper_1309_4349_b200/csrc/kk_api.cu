@@ -51,6 +51,7 @@ cudaError_t launch_band_cluster(const BandParams& P, int64_t replicas, cudaStrea
 int cluster_tb_smem_bytes(const Geom& g, int csize, int TB);
 void set_cluster_tb_layout(BandParams& P, int TB);
 cudaError_t launch_cluster_tb(const BandParams& P, int64_t replicas, int TB, cudaStream_t stream);
+int cluster_max_active(const Geom& g, int csize, int TB);
 int band_tb_smem_bytes(const Geom& g, int nbands, int TB);
 int64_t band_tb_xch_words(const Geom& g, int nbands, int TB);
 cudaError_t launch_band_tb(const BandParams& P, int TB, cudaStream_t stream);
@@ -59,6 +60,12 @@ int resident_threads(const Geom& g, int64_t replicas, int nsm, int forced);
 cudaError_t launch_resident(const ResParams& P, int64_t replicas, int nt, cudaStream_t stream);
 cudaError_t launch_pass(int T, const PassParams& P, const CUtensorMap& tmap, int grid_y, int replicas,
                         cudaStream_t stream, int threads, bool pdl);
+int planar_layout(int T, int THI, int TWI, int NT, PassParams* P);
+cudaError_t launch_planar_pass(int T, const PassParams& P, const CUtensorMap& tmap, int grid_y, int replicas,
+                               cudaStream_t stream, int threads, bool pdl);
+cudaError_t launch_convert(uint32_t* lat, int64_t words, bool to_planar, cudaStream_t s);
+cudaError_t launch_pack_halo_planar(const uint32_t* lat, uint32_t* top, uint32_t* bot, const Geom& g, int64_t replicas,
+                                    int hy, cudaStream_t s);
 cudaError_t launch_observe(const ObsParams& P, cudaStream_t s);
 cudaError_t launch_init_block(uint32_t* lat, const Geom& g, int64_t replicas, int64_t nA, cudaStream_t s);
 cudaError_t launch_select_hist(const Geom& g, int64_t rep0, int64_t nrep, int level, const uint32_t* prefix,
@@ -111,6 +118,8 @@ struct kk_lattice {
     int pass_nt = 512;                // tile kernel CTA size (384, 512 or 640)
     bool tall = false;                // tile kernel: one tall tile per SM at a time (640 threads)
     bool pass_pdl = true;             // programmatic dependent launch of consecutive passes (KK_PDL=0: off)
+    bool planar = false;              // tile passes run the plane-interleaved kernel (kk_planar.cu)
+    bool lay_planar = false;          // buf[cur] currently holds the planar layout (restored lazily)
     int nbands = 0;                   // > 0: kk_sweep runs the band kernel (lattice resident across all SMs)
     int cluster_size = 0;             // > 0: kk_sweep runs the cluster kernel (one cluster per replica)
     int cluster_tb = 1;               // its iterations per halo exchange (1: band_kernel<256, true>)
@@ -155,15 +164,29 @@ int fail(int code, const std::string& msg) {
             return fail(KK_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));  \
     } while (0)
 
-#define KK_CHECK_HANDLE(h)                                                   \
-    do {                                                                     \
-        if (!(h)) return fail(KK_ERR_ARG, "null handle");                    \
-        if ((h)->device >= 0) {                                              \
-            cudaError_t _e = cudaSetDevice((h)->device);                     \
-            if (_e != cudaSuccess)                                           \
+// Makes the handle's device current for the rest of the calling entry point
+// and restores the caller's device on every return path (a process driving
+// handles on several GPUs keeps its own current device).
+struct DeviceGuard {
+    int prev = -1;
+    bool restore = false;
+    ~DeviceGuard() {
+        if (restore) cudaSetDevice(prev);
+    }
+};
+
+#define KK_CHECK_HANDLE(h)                                                                     \
+    if (!(h)) return fail(KK_ERR_ARG, "null handle");                                          \
+    DeviceGuard kk_device_guard_;                                                              \
+    if ((h)->device >= 0) {                                                                    \
+        if (cudaGetDevice(&kk_device_guard_.prev) != cudaSuccess) kk_device_guard_.prev = -1;   \
+        if (kk_device_guard_.prev != (h)->device) {                                            \
+            cudaError_t _e = cudaSetDevice((h)->device);                                       \
+            if (_e != cudaSuccess)                                                             \
                 return fail(KK_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(_e)); \
-        }                                                                    \
-    } while (0)
+            kk_device_guard_.restore = kk_device_guard_.prev >= 0;                             \
+        }                                                                                      \
+    }
 
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
@@ -222,6 +245,8 @@ void set_tiles(kk_lattice* h, int twi_t, int thi_t) {
     h->bands = (int)((rows + thi - 1) / thi);
 }
 
+void set_slab_bands(kk_lattice* h);
+
 void choose_tiles(kk_lattice* h, int nsm) {
     const int twi_env = env_int("KK_TWI", 0), thi_env = env_int("KK_THI", 0);
     if (twi_env > 0 || thi_env > 0) {
@@ -267,13 +292,67 @@ void choose_tiles(kk_lattice* h, int nsm) {
         }
         set_tiles(h, bt, bh);
     }
+    set_slab_bands(h);
+}
+
+// slab mode: bands whose loaded rows [b*THI - hy, (b+1)*THI + hy) are local
+void set_slab_bands(kk_lattice* h) {
     const int64_t rows = h->g.rows, thi = h->THI;
-    // slab mode: bands whose loaded rows [b*THI - hy, (b+1)*THI + hy) are local
     h->b_lo = (int)((h->hy + thi - 1) / thi);
     h->b_hi = (int)std::max<int64_t>(0, (rows - h->hy) / thi);
     if (h->b_hi < h->b_lo) h->b_hi = h->b_lo;
     if (h->b_hi > h->bands) h->b_hi = h->bands;
     if (h->b_lo > h->bands) h->b_lo = h->b_hi = h->bands;
+}
+
+// Tile shape of the planar kernel (one CTA of pass_nt threads per SM; tile
+// widths are whole 128-site groups).  Cost model per CTA: the item rounds of
+// the T iterations (interior rows + the light cone, ~1.5 rows per remaining
+// iteration on each side, R8; items = centre rows x (groups + 2 halo
+// groups); a round = pass_nt items) plus staging and a fixed cost; the grid
+// runs in waves of one CTA per SM.  KK_TWI / KK_THI force the targets.
+void choose_tiles_planar(kk_lattice* h, int nsm) {
+    const int T = h->T, NT = h->pass_nt;
+    const int twi_env = env_int("KK_TWI", 0), thi_env = env_int("KK_THI", 0);
+    auto set_planar = [&](int twi, int thi) {
+        const int64_t Wg = h->g.W / 4, rows = h->g.rows;
+        const int64_t G = std::max<int64_t>(1, std::min<int64_t>(Wg, twi / 4));
+        const int64_t nx = (Wg + G - 1) / G;
+        h->TWI = (int)(4 * ((Wg + nx - 1) / nx));
+        h->tiles_x = (int)((Wg * 4 + h->TWI - 1) / h->TWI);
+        const int64_t nb = (rows + thi - 1) / thi;
+        int64_t t = (rows + nb - 1) / nb;
+        t = (t + 3) / 4 * 4;
+        h->THI = (int)t;
+        h->bands = (int)((rows + t - 1) / t);
+    };
+    if (twi_env > 0 || thi_env > 0) {
+        set_planar(std::max(4, twi_env > 0 ? twi_env : 64), std::max(4, thi_env > 0 ? thi_env : 596));
+        return;
+    }
+    double best = 1e300;
+    int bt = 64, bh = 596;
+    for (int twi : {16, 32, 64, 128}) {
+        for (int thi = 8; thi <= 2048; thi += 4) {
+            set_planar(twi, thi);
+            if (planar_layout(T, h->THI, h->TWI, NT, nullptr) > 227 * 1024) break;
+            const int NG = h->TWI / 4 + 2;
+            double work = 0.0;
+            for (int t = 0; t < T; ++t) {
+                const double rows = (h->THI + 3.0 * (T - 1 - t) + 2.0) / 4.0;
+                work += std::ceil(std::ceil(rows) * NG / NT);
+            }
+            work += 0.25 * (double)(h->THI + 6 * T) * NG / NT + 2.0;  // staging + fixed
+            const int64_t ctas = (int64_t)h->tiles_x * h->bands * h->R;
+            const double t = (double)((ctas + nsm - 1) / nsm) * work;
+            if (t < best * 0.999) {
+                best = t;
+                bt = h->TWI;
+                bh = h->THI;
+            }
+        }
+    }
+    set_planar(bt, bh);
 }
 
 PassParams make_pass_params(kk_lattice* h, const uint32_t* ht, const uint32_t* hb) {
@@ -297,7 +376,13 @@ PassParams make_pass_params(kk_lattice* h, const uint32_t* ht, const uint32_t* h
         P.rk[10 + r] = P.key1 + (uint32_t)r * 0xBB67AE85u;
     }
     for (int k = 0; k < 7; ++k) P.thr[k] = h->thr[k];
-    set_pass_layout(h->T, P);
+    // planar kernel: thresholds by |v| on the side that needs a draw (R5)
+    P.need_dn = h->omega < 0.0 ? 1 : 0;
+    P.thm[0] = 0xFFFFFFFFu;
+    for (int m = 1; m <= 3; ++m) P.thm[m] = h->thr[P.need_dn ? 3 - m : 3 + m];
+    P.need_any = P.thm[3] != 0xFFFFFFFFu ? 1 : 0;
+    if (h->planar) planar_layout(h->T, h->THI, h->TWI, h->pass_nt, &P);
+    else set_pass_layout(h->T, P);
     P.use_tma = h->use_tma;
     P.box_h = h->box_h;
     P.vec_wb = (h->g.tail == 0 && h->g.W % 4 == 0 && h->TWI % 4 == 0) ? 1 : 0;
@@ -306,12 +391,30 @@ PassParams make_pass_params(kk_lattice* h, const uint32_t* ht, const uint32_t* h
 
 // TMA descriptors for the two lattice buffers: a 3D uint32 tensor
 // (W words, rows, replicas) read in boxes of (TWI + 8) words x box_h rows.
+// TMA staging plan (host logic): boxes of WS = TWI + 8 words x box_h rows per
+// tile, or 0 when the lattice / tile shape does not allow it (row tail, W or
+// WS not a multiple of 4 words, WS > 256, or a box whose first row would not
+// start 128-byte aligned in shared memory, as cp.async.bulk.tensor requires).
+int tma_boxes(const kk_lattice* h, int* box_h_out) {
+    const int WS = h->TWI + 8, H = h->THI + 6 * h->T;
+    if (h->g.tail != 0 || h->g.W % 4 != 0 || WS % 4 != 0 || WS > 256 || !env_int("KK_TMA", 1)) return 0;
+    const int box_h = std::min(256, H);
+    const int nbox = (H + box_h - 1) / box_h;
+    for (int b = 0; b < nbox; ++b) {
+        const int y0 = std::min(b * box_h, H - box_h);
+        if (((int64_t)y0 * WS * 4) % 128 != 0) return 0;
+    }
+    if (box_h_out) *box_h_out = box_h;
+    return nbox;
+}
+
 void make_tensor_maps(kk_lattice* h) {
     h->use_tma = 0;
-    const int WS = h->TWI + 8, H = h->THI + 6 * h->T;
+    const int WS = h->TWI + 8;
     // TMA staging of interior tiles (default; KK_TMA=0 selects the LDG path):
     // +6% on the 65536^2 bench lattice (tools/tma_rate.py).
-    if (h->g.tail != 0 || h->g.W % 4 != 0 || WS % 4 != 0 || WS > 256 || !env_int("KK_TMA", 1)) return;
+    int box_h = 0;
+    if (!tma_boxes(h, &box_h)) return;
     PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode), cudaEnableDefault,
@@ -319,7 +422,7 @@ void make_tensor_maps(kk_lattice* h) {
         cudaGetLastError();
         return;
     }
-    h->box_h = std::min(256, H);
+    h->box_h = box_h;
     const cuuint64_t dims[3] = {(cuuint64_t)h->g.W, (cuuint64_t)h->g.rows, (cuuint64_t)h->R};
     const cuuint64_t strides[2] = {(cuuint64_t)h->g.W * 4, (cuuint64_t)h->g.rows * h->g.W * 4};
     const cuuint32_t box[3] = {(cuuint32_t)WS, (cuuint32_t)h->box_h, 1};
@@ -331,6 +434,16 @@ void make_tensor_maps(kk_lattice* h) {
         if (r != CUDA_SUCCESS) return;
     }
     h->use_tma = 1;
+}
+
+// The planar kernel keeps buf[cur] in the plane-interleaved layout between
+// passes; every call that reads or writes the lattice in the public layout
+// converts it back first (in place, stream-ordered on the caller's stream).
+int ensure_layout(kk_lattice* h, bool planar, cudaStream_t s) {
+    if (h->lay_planar == planar) return KK_OK;
+    KK_CUDA(launch_convert(h->buf[h->cur], (int64_t)h->R * h->g.rep_words, planar, s));
+    h->lay_planar = planar;
+    return KK_OK;
 }
 
 int run_pass(kk_lattice* h, int region, const uint32_t* ht, const uint32_t* hb, cudaStream_t s) {
@@ -347,6 +460,12 @@ int run_pass(kk_lattice* h, int region, const uint32_t* ht, const uint32_t* hb, 
         grid_y = h->b_lo + (h->bands - h->b_hi);
     } else {
         return fail(KK_ERR_ARG, "kk_pass: bad region");
+    }
+    if (h->planar) {
+        int rc = ensure_layout(h, true, s);
+        if (rc != KK_OK) return rc;
+        KK_CUDA(launch_planar_pass(h->T, P, h->tmap[h->cur], grid_y, (int)h->R, s, h->pass_nt, h->pass_pdl));
+        return KK_OK;
     }
     KK_CUDA(launch_pass(h->T, P, h->tmap[h->cur], grid_y, (int)h->R, s, h->pass_nt, h->pass_pdl));  // grid.z = replica (R <= 65535)
     return KK_OK;
@@ -658,6 +777,22 @@ int plan_handle(kk_lattice* h, const kk_config* c, int T, int nsm) {
         h->resident = 0;
         h->nbands = 0;
     }
+    // planar tile kernel (kk_planar.cu): rows of whole 128-site groups
+    // (Lx % 128 == 0); KK_PLANAR=0 keeps the row-major tile kernel.
+    h->planar = !h->cluster_size && !h->nbands && !h->resident && h->g.tail == 0 && h->g.W % 4 == 0 &&
+                env_int("KK_PLANAR", 1) != 0;
+    if (h->planar) {
+        const int forced = env_int("KK_PASS_THREADS", 0);
+        h->pass_nt = (forced == 512 || forced == 640 || forced == 768 || forced == 896) ? forced : 640;
+        choose_tiles_planar(h, nsm);
+        set_slab_bands(h);
+        const int64_t ctas = (int64_t)h->tiles_x * h->bands * h->R;
+        const int pdl = env_int("KK_PDL", -1);
+        h->pass_pdl = pdl < 0 ? ctas <= (int64_t)nsm : pdl != 0;
+        if (planar_layout(T, h->THI, h->TWI, h->pass_nt, nullptr) > 227 * 1024)
+            return fail(KK_ERR_ARG, "planar tile too large for shared memory (KK_THI/KK_TWI)");
+        return KK_OK;
+    }
     if (pass_smem_bytes(T, h->THI, h->TWI) > 227 * 1024)
         return fail(KK_ERR_ARG, "tile too large for shared memory (KK_THI/KK_TWI)");
     return KK_OK;
@@ -693,14 +828,21 @@ int kk_plan_config(const kk_config* c, int n_sm, kk_plan* out) {
     out->kernel = tmp.cluster_size ? KK_KERNEL_CLUSTER
                   : tmp.nbands      ? KK_KERNEL_BAND
                   : tmp.resident    ? KK_KERNEL_RESIDENT
+                  : tmp.planar      ? KK_KERNEL_PLANAR
                                     : KK_KERNEL_TILE;
     out->iters_per_pass = T;
+    out->tma_boxes = (out->kernel == KK_KERNEL_TILE || out->kernel == KK_KERNEL_PLANAR) ? tma_boxes(&tmp, nullptr) : 0;
     out->tile_rows = tmp.THI;
     out->tile_words = tmp.TWI;
     out->tiles_x = tmp.tiles_x;
     out->bands = tmp.bands;
     out->halo_rows = tmp.hy;
-    if (out->kernel == KK_KERNEL_TILE) {
+    if (out->kernel == KK_KERNEL_PLANAR) {
+        out->threads = tmp.pass_nt;
+        out->pass_pdl = tmp.pass_pdl ? 1 : 0;
+        out->smem_bytes = planar_layout(T, tmp.THI, tmp.TWI, tmp.pass_nt, nullptr);
+        out->ctas = (int64_t)tmp.tiles_x * tmp.bands * tmp.R;
+    } else if (out->kernel == KK_KERNEL_TILE) {
         out->threads = tmp.pass_nt;
         out->pass_pdl = tmp.pass_pdl ? 1 : 0;
         out->smem_bytes = pass_smem_bytes(T, tmp.THI, tmp.TWI);
@@ -740,6 +882,19 @@ int kk_create_ex(kk_handle* out, const kk_config* c) {
     if (rc0 != KK_OK) {
         delete h;
         return rc0;
+    }
+    // 16-CTA (non-portable) clusters need a GPC with 16 free SMs for this
+    // shared-memory size: check the device can hold every replica's cluster
+    // at once, else fall back to 8-CTA clusters (same results, R4/R8)
+    if (h->cluster_size == 16 && env_int("KK_CLUSTER", -1) < 0 &&
+        cluster_max_active(h->g, 16, h->cluster_tb) < h->R && cluster_smem_bytes(h->g, 8) > 0) {
+        h->cluster_size = 8;
+        h->cluster_tb = 1;
+        for (int tb : {4, 2})
+            if (cluster_tb_smem_bytes(h->g, 8, tb) > 0) {
+                h->cluster_tb = tb;
+                break;
+            }
     }
     const size_t words = (size_t)h->R * (size_t)h->g.rep_words;
     cudaError_t e1 = cudaMalloc(&h->buf[0], words * 4);
@@ -802,8 +957,10 @@ int kk_create(kk_handle* out, int64_t Lx, int64_t Ly, double fraction_A, double 
 
 int kk_destroy(kk_handle h) {
     if (!h) return KK_OK;
-    if (h->device >= 0) cudaSetDevice(h->device);
-    cudaDeviceSynchronize();
+    KK_CHECK_HANDLE(h);
+    // No explicit device-wide barrier: cudaFree does not return before the
+    // device work that may still use these buffers has finished (its own
+    // implicit synchronisation), so nothing else is needed here.
     free_all(h);
     delete h;
     return KK_OK;
@@ -917,12 +1074,25 @@ int kk_sweep(kk_handle h, int64_t n, void* stream) {
 
 int kk_pack_halo(kk_handle h, uint32_t* send_top, uint32_t* send_bot, void* stream) {
     KK_CHECK_HANDLE(h);
+    if (h->planar) {
+        // the next pass runs planar: convert now (on this stream, before the
+        // caller forks its interior pass onto a side stream); the halo rows
+        // are written in the public row-major layout
+        int rc = ensure_layout(h, true, S(stream));
+        if (rc != KK_OK) return rc;
+        KK_CUDA(launch_pack_halo_planar(h->buf[h->cur], send_top, send_bot, h->g, h->R, h->hy, S(stream)));
+        return KK_OK;
+    }
     KK_CUDA(launch_pack_halo(h->buf[h->cur], send_top, send_bot, h->g, h->R, h->hy, S(stream)));
     return KK_OK;
 }
 
 int kk_energy(kk_handle h, int64_t* nab_out, double* energy_out, const uint32_t* halo_bot, void* stream) {
     KK_CHECK_HANDLE(h);
+    {
+        int rc_l = ensure_layout(h, false, S(stream));
+        if (rc_l != KK_OK) return rc_l;
+    }
     if (!nab_out) return fail(KK_ERR_ARG, "nab_out is null");
     cudaStream_t s = S(stream);
     KK_CUDA(cudaMemsetAsync(h->obs, 0, sizeof(unsigned long long) * 2 * h->R, s));
@@ -946,6 +1116,10 @@ int kk_energy(kk_handle h, int64_t* nab_out, double* energy_out, const uint32_t*
 
 int kk_composition(kk_handle h, int64_t* na_out, void* stream) {
     KK_CHECK_HANDLE(h);
+    {
+        int rc_l = ensure_layout(h, false, S(stream));
+        if (rc_l != KK_OK) return rc_l;
+    }
     if (!na_out) return fail(KK_ERR_ARG, "na_out is null");
     cudaStream_t s = S(stream);
     KK_CUDA(cudaMemsetAsync(h->obs, 0, sizeof(unsigned long long) * 2 * h->R, s));
@@ -1068,6 +1242,10 @@ extern "C" {
 
 int kk_cluster_histogram(kk_handle h, int target, int64_t* out, int64_t capacity, int64_t* n_out, void* stream) {
     KK_CHECK_HANDLE(h);
+    {
+        int rc_l = ensure_layout(h, false, S(stream));
+        if (rc_l != KK_OK) return rc_l;
+    }
     if (!n_out) return fail(KK_ERR_ARG, "n_out is null");
     if (!h->g.periodic) return fail(KK_ERR_STATE, "cluster histogram needs a full-lattice handle (kk_cluster_slab)");
     cudaStream_t s = S(stream);
@@ -1091,6 +1269,10 @@ int kk_cluster_slab(kk_handle h, int target, int64_t* hist_out, int64_t capacity
                     uint32_t* top_ids, uint32_t* bot_ids, unsigned long long* open_sizes, int64_t open_cap,
                     int64_t* n_open, void* stream) {
     KK_CHECK_HANDLE(h);
+    {
+        int rc_l = ensure_layout(h, false, S(stream));
+        if (rc_l != KK_OK) return rc_l;
+    }
     if (!n_hist || !n_open || !top_ids || !bot_ids || !open_sizes) return fail(KK_ERR_ARG, "null argument");
     if (h->R != 1) return fail(KK_ERR_STATE, "kk_cluster_slab: one replica per handle");
     cudaStream_t s = S(stream);
@@ -1166,6 +1348,10 @@ int kk_cluster_join(int64_t Lx, int64_t nslabs, const uint32_t* top_ids, const u
 
 int kk_get_lattice(kk_handle h, uint8_t* out, void* stream) {
     KK_CHECK_HANDLE(h);
+    {
+        int rc_l = ensure_layout(h, false, S(stream));
+        if (rc_l != KK_OK) return rc_l;
+    }
     if (!out) return fail(KK_ERR_ARG, "out is null");
     cudaStream_t s = S(stream);
     const size_t n = (size_t)h->R * h->g.rows * h->g.Lx;
@@ -1179,6 +1365,7 @@ int kk_get_lattice(kk_handle h, uint8_t* out, void* stream) {
 
 int kk_set_lattice(kk_handle h, const uint8_t* in, void* stream) {
     KK_CHECK_HANDLE(h);
+    h->lay_planar = false;
     if (!in) return fail(KK_ERR_ARG, "in is null");
     cudaStream_t s = S(stream);
     const size_t n = (size_t)h->R * h->g.rows * h->g.Lx;
@@ -1192,6 +1379,10 @@ int kk_set_lattice(kk_handle h, const uint8_t* in, void* stream) {
 
 int kk_get_lattice_packed(kk_handle h, uint32_t* out, void* stream) {
     KK_CHECK_HANDLE(h);
+    {
+        int rc_l = ensure_layout(h, false, S(stream));
+        if (rc_l != KK_OK) return rc_l;
+    }
     if (!out) return fail(KK_ERR_ARG, "out is null");
     const size_t bytes = (size_t)h->R * h->g.rep_words * 4;
     KK_CUDA(cudaMemcpyAsync(out, h->buf[h->cur], bytes, cudaMemcpyDeviceToHost, S(stream)));
@@ -1201,6 +1392,7 @@ int kk_get_lattice_packed(kk_handle h, uint32_t* out, void* stream) {
 
 int kk_set_lattice_packed(kk_handle h, const uint32_t* in, void* stream) {
     KK_CHECK_HANDLE(h);
+    h->lay_planar = false;
     if (!in) return fail(KK_ERR_ARG, "in is null");
     const size_t bytes = (size_t)h->R * h->g.rep_words * 4;
     KK_CUDA(cudaMemcpyAsync(h->buf[h->cur], in, bytes, cudaMemcpyHostToDevice, S(stream)));
@@ -1214,9 +1406,12 @@ int kk_copy_lattice_packed_device(kk_handle h, uint32_t* dst, int to_device_buff
     const size_t bytes = (size_t)h->R * h->g.rep_words * 4;
     if (to_device_buffer) {
         if (!src) return fail(KK_ERR_ARG, "src is null");
+        h->lay_planar = false;
         KK_CUDA(cudaMemcpyAsync(h->buf[h->cur], src, bytes, cudaMemcpyDeviceToDevice, S(stream)));
     } else {
         if (!dst) return fail(KK_ERR_ARG, "dst is null");
+        int rc = ensure_layout(h, false, S(stream));
+        if (rc != KK_OK) return rc;
         KK_CUDA(cudaMemcpyAsync(dst, h->buf[h->cur], bytes, cudaMemcpyDeviceToDevice, S(stream)));
     }
     return KK_OK;
@@ -1238,6 +1433,7 @@ int kk_init_select_ties(kk_handle h, const uint32_t* K, int64_t* out, int64_t ca
 int kk_init_select_apply(kk_handle h, const uint32_t* K, const int64_t* cut, void* stream) {
     KK_CHECK_HANDLE(h);
     if (!K || !cut) return fail(KK_ERR_ARG, "null argument");
+    h->lay_planar = false;  // every word is rewritten in the public layout
     return select_apply(h, K, cut, S(stream));
 }
 

@@ -40,13 +40,12 @@
 // (north_star part 4; R5).  Flips are XOR masks applied with shared-memory
 // atomics (bits of different centres are disjoint, so the XORs commute and
 // the result does not depend on thread scheduling).
-#include <cuda.h>  // CUtensorMap (TMA descriptor type only; no driver calls here)
-
 #include <algorithm>
 
 #include <cooperative_groups.h>
 
 #include "kk_internal.cuh"
+#include "kk_device.cuh"
 
 namespace kk {
 
@@ -72,57 +71,6 @@ __device__ __forceinline__ uint32_t nib_view(uint32_t left, uint32_t mid, uint32
         v = __funnelshift_l(left, mid, -s);
     }
     return v & kNib;
-}
-
-// N independent Philox4x32-10 streams (counters m[k], c1, c2, c3), rounds
-// interleaved for ILP; the round keys come precomputed from the parameter bank
-// (rk[0..9] for key word 0, rk[10..19] for key word 1), so no per-item key
-// schedule is issued.
-template <int N>
-__device__ __forceinline__ void philox10_xn(const uint32_t m[N], uint32_t c1, uint32_t c2, uint32_t c3,
-                                            const uint32_t* rk, uint32_t out[N][4]) {
-    uint32_t a[N], b[N], c[N], d[N];
-#pragma unroll
-    for (int p = 0; p < N; ++p) {
-        a[p] = m[p];
-        b[p] = c1;
-        c[p] = c2;
-        d[p] = c3;
-    }
-#pragma unroll
-    for (int round = 0; round < 10; ++round) {
-#pragma unroll
-        for (int p = 0; p < N; ++p) {
-            const uint64_t p0 = (uint64_t)kPhiloxM0 * a[p];
-            const uint64_t p1 = (uint64_t)kPhiloxM1 * c[p];
-            const uint32_t na = (uint32_t)(p1 >> 32) ^ b[p] ^ rk[round];
-            const uint32_t nc = (uint32_t)(p0 >> 32) ^ d[p] ^ rk[10 + round];
-            b[p] = (uint32_t)p1;
-            d[p] = (uint32_t)p0;
-            a[p] = na;
-            c[p] = nc;
-        }
-    }
-#pragma unroll
-    for (int p = 0; p < N; ++p) {
-        out[p][0] = a[p];
-        out[p][1] = b[p];
-        out[p][2] = c[p];
-        out[p][3] = d[p];
-    }
-}
-
-// acc | bit if u <= t: a compare and a predicated OR (the compiler's own
-// select + add form costs a third more ALU-pipe instructions).
-__device__ __forceinline__ uint32_t or_if_le(uint32_t acc, uint32_t u, uint32_t t, uint32_t bit) {
-    uint32_t r;
-    asm("{\n\t.reg .pred p;\n\t"
-        "setp.le.u32 p, %1, %2;\n\t"
-        "mov.b32 %0, %3;\n\t"
-        "@p or.b32 %0, %3, %4;\n\t}"
-        : "=r"(r)
-        : "r"(u), "r"(t), "r"(acc), "r"(bit));
-    return r;
 }
 
 // w[i] for a runtime i in 0..3 without local-memory indexing.
@@ -158,43 +106,6 @@ extern __shared__ __align__(128) uint32_t kk_smem[];
 // No static __shared__ variables in the pass kernel: the dynamic region then
 // starts at the beginning of the CTA's shared window, which keeps the tile
 // 128-byte aligned for the TMA destination.
-
-// ---- programmatic dependent launch (no-ops when the grid was launched without it)
-__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-
-// ---- TMA (cp.async.bulk.tensor) staging of interior tiles ----------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n"
-        "LAB_WAIT:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@P1 bra DONE;\n\t"
-        "bra LAB_WAIT;\n"
-        "DONE:\n\t}" ::"r"(smem_u32(bar)),
-        "r"(phase)
-        : "memory");
-}
-
-__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint64_t* bar, int x, int y, int z) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-        "[%5];" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
-        : "memory");
-}
 
 struct Tabs {
     int mt_off;                // uint2 [Wt]: (global x of bit 0, word holds one aligned octet of centres)
@@ -411,21 +322,6 @@ __device__ __forceinline__ void process_item(const Tabs& S, int r, int w, uint32
     const uint32_t Sg = idx & (A * 15u);
     acc.idx_even += Sg & 0x0F0F0F0Fu;   // byte lanes: <= 6 per item per lane
     acc.idx_odd += (Sg >> 4) & 0x0F0F0F0Fu;
-}
-
-// A thread's walk over a (rows x W) grid in steps of NT: start (a0, w0) and
-// step (da, dw), computed once per kernel so the loops issue no division.
-struct Walk {
-    int a0, w0, da, dw;
-};
-template <int NT>
-__device__ __forceinline__ Walk make_walk(int W) {
-    Walk k;
-    k.a0 = (int)threadIdx.x / W;
-    k.w0 = (int)threadIdx.x - k.a0 * W;
-    k.da = NT / W;
-    k.dw = NT - k.da * W;
-    return k;
 }
 
 template <int KX, bool FAST, int NT>
@@ -1744,6 +1640,43 @@ cudaError_t launch_cluster_tb(const BandParams& P, int64_t replicas, int TB, cud
     if (e != cudaSuccess) return e;
     count_launch();
     return cudaGetLastError();
+}
+
+// Clusters of csize CTAs (the cluster kernel's launch shape) that the device
+// can hold at once; 0 if the shape cannot be resident (e.g. a 16-CTA
+// non-portable cluster on a floor-swept part or a MIG slice).
+int cluster_max_active(const Geom& g, int csize, int TB) {
+    const int smem = TB > 1 ? cluster_tb_smem_bytes(g, csize, TB) : cluster_smem_bytes(g, csize);
+    if (!smem) return 0;
+    const void* fn = TB == 2   ? (const void*)cluster_kernel<kClusterThreads, 2, false>
+                     : TB == 4 ? (const void*)cluster_kernel<kClusterThreads, 4, false>
+                     : TB == 8 ? (const void*)cluster_kernel<kClusterThreads, 8, false>
+                               : (const void*)band_kernel<kClusterThreads, true>;
+    if (ensure_dynamic_smem(fn, smem) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    if (csize > 8 && cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)csize);
+    cfg.blockDim = dim3(kClusterThreads);
+    cfg.dynamicSmemBytes = (size_t)smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)csize;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
 }
 
 // Band kernel with temporal blocking (L2 exchange every TB iterations).

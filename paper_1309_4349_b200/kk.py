@@ -40,10 +40,11 @@ class Plan(ctypes.Structure):
     _fields_ = [("kernel", ctypes.c_int32), ("iters_per_pass", ctypes.c_int32), ("tile_rows", ctypes.c_int32),
                 ("tile_words", ctypes.c_int32), ("tiles_x", ctypes.c_int32), ("bands", ctypes.c_int32),
                 ("halo_rows", ctypes.c_int32), ("threads", ctypes.c_int32), ("smem_bytes", ctypes.c_int32),
-                ("pass_pdl", ctypes.c_int32), ("ctas", ctypes.c_int64)]
+                ("pass_pdl", ctypes.c_int32), ("ctas", ctypes.c_int64), ("tma_boxes", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
 
 
-KERNEL_NAMES = {0: "tile", 1: "resident", 2: "band", 3: "cluster"}
+KERNEL_NAMES = {0: "tile", 1: "resident", 2: "band", 3: "cluster", 4: "planar"}
 
 
 # symbol -> (restype, argtypes); the ABI surface declared in include/kk.h
