@@ -45,7 +45,12 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--Lx", type=int, default=65536)
-    p.add_argument("--rows-per-gpu", type=int, default=65536)
+    p.add_argument("--rows-per-gpu", type=int, default=0,
+                   help="rows per rank (default: 65536 for --scaling weak, 65536/N for strong)")
+    p.add_argument("--scaling", choices=["weak", "strong", "both"], default="both",
+                   help="weak: a 65536-row slab per GPU (the headline line); strong: one 65536^2 lattice "
+                        "split over the N GPUs; both (default): the weak line, and at N > 1 the strong run "
+                        "attached to it as 'strong_scaling'")
     p.add_argument("--sweeps-per-step", type=int, default=100)
     p.add_argument("--omega", type=float, default=0.6)
     p.add_argument("--fraction", type=float, default=0.5)
@@ -151,14 +156,22 @@ def measured_peaks():
         return 6650.0, 1965.0, "fallback"
 
 
-def kernel_counters():
-    """Per-site-update instruction count and DRAM bytes of the pass kernel from
-    the committed ncu capture (profiles/pass_kernel_counters.json)."""
+def kernel_counters(plan: dict):
+    """Per-site-update instruction count, pipe utilisation and DRAM bytes of the
+    pass kernel from the committed ncu capture of the bench lattice
+    (profiles/pass_kernel_counters.json, tools/write_counters.py) — only if it
+    was captured with exactly this run's launch plan (kernel, T, tile shape,
+    CTA size, TMA boxes); a stale capture is refused (None, reason)."""
     try:
         with open(os.path.join(ROOT, "profiles", "pass_kernel_counters.json")) as f:
-            return json.load(f)
-    except Exception:
-        return None
+            cnt = json.load(f)
+    except Exception as e:  # noqa: BLE001
+        return None, f"no counters file ({e.__class__.__name__})"
+    want = {k: plan[k] for k in ("kernel", "iters_per_pass", "tile_words", "tile_rows", "threads", "tma_boxes")}
+    got = cnt.get("plan", {})
+    if any(got.get(k) != v for k, v in want.items()):
+        return None, f"counters captured for plan {got}, this run uses {want}"
+    return cnt, None
 
 
 # ------------------------------------------------------------------------ CPU baseline
@@ -241,7 +254,34 @@ def main():
     from paper_1309_4349_b200 import kk
     from paper_1309_4349_b200 import distributed as D
 
-    rows = a.rows_per_gpu
+    ctx = dict(a=a, torch=torch, dist=dist, backend=backend, kk=kk, D=D, rank=rank, world=world, local=local)
+    if a.scaling == "strong":
+        rows = a.rows_per_gpu or max(4, 65536 // world)
+        out = measure(ctx, rows, "strong", with_e2e=not a.no_e2e)
+    else:
+        out = measure(ctx, a.rows_per_gpu or 65536, "weak", with_e2e=not a.no_e2e)
+        if a.scaling == "both" and world > 1:
+            strong = measure(ctx, max(4, 65536 // world), "strong", with_e2e=False)
+            if out is not None:
+                out["strong_scaling"] = {k: strong[k] for k in ("value", "unit", "ms_per_step", "config",
+                                                                 "roofline", "gpu_launches", "clocks")}
+    if rank == 0:
+        if world == 1 and not a.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(a.cpu_seconds, a.omega, a.fraction, a.seed)
+        if world == 1 and not a.no_other_configs:
+            out["other_configs"] = other_configs(torch)
+        print(json.dumps(out), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def measure(ctx, rows, scaling, with_e2e=True):
+    """One bench configuration: `rows` rows per rank of a Lx x (rows * N)
+    torus; W warm-up steps, K timed steps (CUDA events, max over ranks), the
+    pass kernel's roofline from per-launch events, and the end-to-end run
+    through the C ABI's host I/O.  Returns the JSON dict on rank 0."""
+    a, torch, dist, backend, kk, D = ctx["a"], ctx["torch"], ctx["dist"], ctx["backend"], ctx["kk"], ctx["D"]
+    rank, world, local = ctx["rank"], ctx["world"], ctx["local"]
     Lx, Ly = a.Lx, rows * world
     stream = torch.cuda.current_stream()
     sim = D.make_simulation(Lx, Ly, a.fraction, a.omega, a.seed, T=a.T, world=world, rank=rank,
@@ -270,6 +310,7 @@ def main():
     torch.cuda.synchronize()
     launches0 = kk.launch_count()
     hbm_peak, sm_max_mhz, peak_src = measured_peaks()
+    peak_src_hbm = peak_src
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -294,50 +335,63 @@ def main():
     updates_per_step = a.sweeps_per_step * Lx * Ly  # all ranks
     value = updates_per_step * a.steps / (ms / 1e3)
 
-    # ---- roofline of the dominant kernel (pass_kernel), from live event timings
+    # ---- roofline of the dominant kernel (the pass kernel), from live event timings
     pass_avg_s = float(np.mean(pass_ms)) / 1e3
     upd_per_launch = N_local * a.T / 16
     hbm_bytes_per_launch = 2 * N_local / 8  # read + write every site bit once (algorithmic)
     hbm_achieved = hbm_bytes_per_launch / pass_avg_s / 1e9
-    cnt = kernel_counters()
-    alu_peak = 148 * 128 * sm_max_mhz * 1e6 / 1e12  # lane-ops/s: 148 SM x 128 INT/FP32 lanes x clock
-    if cnt and cnt.get("T") == a.T:
+    n_sm = torch.cuda.get_device_properties(local).multi_processor_count
+    plan = kk.plan(Lx, Ly, y_begin=rank * rows, y_count=rows, iters_per_pass=a.T, n_sm=n_sm)
+    kname = {"planar": "planar_pass_kernel", "tile": "pass_kernel"}.get(plan["kernel"], plan["kernel"])
+    cnt, why = kernel_counters(plan)
+    # issue peak: n_SM x 4 SMSPs x 32 lanes x 1 warp-instruction / clk at the max SM clock
+    alu_peak = n_sm * 128 * sm_max_mhz * 1e6 / 1e12
+    peak_src = f"{n_sm} SMs x 128 lanes x {sm_max_mhz:.0f} MHz (max SM clock, {peak_src})"
+    upd_rate = upd_per_launch / pass_avg_s
+    # implementation-independent floor: the Philox work R6
+    # fixes (3 Philox4x32-10 calls per 8 centres, 10 rounds x 2 wide
+    # multiplies + 2 three-way XORs = 40 integer ops a call: 15 ops / update)
+    floor = 15.0
+    roof = {"bound": "alu", "unit": "Tlane-op/s", "peak": alu_peak, "peak_source": peak_src,
+            "kernel": kname, "plan": {k: plan[k] for k in ("kernel", "tile_words", "tile_rows", "threads",
+                                                          "tma_boxes", "ctas")},
+            "launch_ms": pass_avg_s * 1e3, "updates_per_launch": upd_per_launch,
+            "ops_floor_per_update": floor, "floor_frac": floor * upd_rate / 1e12 / alu_peak}
+    if cnt:
         lane_ops = cnt["thread_inst_per_update"] * upd_per_launch
         achieved = lane_ops / pass_avg_s / 1e12
         traffic = cnt.get("dram_bytes_per_update")
-        traffic = traffic * upd_per_launch if traffic is not None else None
-        roof = {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "Tlane-op/s",
-                "frac": achieved / alu_peak, "traffic": traffic,
-                "peak_source": f"148 SMs x 128 lanes x {sm_max_mhz:.0f} MHz (max SM clock, {peak_src})",
-                "per_launch_ops": lane_ops, "ops_source": cnt.get("source")}
+        roof.update({"achieved": achieved, "frac": achieved / alu_peak,
+                     "traffic": traffic * upd_per_launch if traffic is not None else None,
+                     "per_launch_ops": lane_ops, "thread_inst_per_update": cnt["thread_inst_per_update"],
+                     "alu_pipe_frac": cnt.get("alu_pipe_pct", 0) / 100.0,
+                     "fma_pipe_frac": cnt.get("fma_pipe_pct", 0) / 100.0,
+                     "issue_active_frac": cnt.get("issue_active_pct", 0) / 100.0,
+                     "ops_source": cnt.get("source")})
     else:
-        roof = {"bound": "alu", "achieved": None, "peak": alu_peak, "unit": "Tlane-op/s",
-                "frac": None, "traffic": None, "note": "no ncu counters for this T yet"}
-    roof["kernel"] = "pass_kernel"
-    roof["launch_ms"] = pass_avg_s * 1e3
+        roof.update({"achieved": None, "frac": None, "traffic": None, "note": why})
     roof["share_of_step"] = float(np.sum(pass_ms)) / (ms / 1.0) if ms > 0 else None
     roof["hbm"] = {"achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s",
                    "frac": hbm_achieved / hbm_peak, "bytes_per_launch": hbm_bytes_per_launch,
-                   "peak_source": peak_src}
+                   "peak_source": peak_src_hbm}
 
     # ---- end to end through the public API: H2D of the step's lattice from pinned
     # host memory, the step, D2H of the observables (and of the lattice)
     e2e = None
-    if not a.no_e2e:
-        # Every step: H2D of the step's input lattice from pinned host memory,
-        # the step, D2H of its result lattice (+ the observables).  The copies
-        # run on a copy stream through device staging buffers, so step k+1's
-        # upload and step k's download overlap step k's / k+1's sweeps; the
-        # lattice itself is loaded / saved with on-device copies.
+    if with_e2e:
+        # Every step, through the library's double-buffered host I/O (C ABI,
+        # include/kk.h): upload of the step's input lattice from pinned host
+        # memory (kk_upload_packed_async on a copy stream, overlapping the
+        # previous step; kk_commit_upload on the compute stream), the step,
+        # and the download of its result (kk_snapshot + kk_download_packed_async,
+        # overlapping the next step; the last one inside the timed region).
         words = sim.packed_words()
         host_in = torch.empty(words, dtype=torch.int32, pin_memory=True)
         host_out = torch.empty(words, dtype=torch.int32, pin_memory=True)
-        stage_in = torch.empty(words, dtype=torch.int32, device="cuda")
-        stage_out = torch.empty(words, dtype=torch.int32, device="cuda")
-        sim.download_packed(host_in.data_ptr())
-        torch.cuda.synchronize()
+        sim.snapshot(stream)
         cp = torch.cuda.Stream()
-        ev = lambda: torch.cuda.Event()  # noqa: E731
+        sim.download_async(host_in.data_ptr(), cp)      # the current state is the first input
+        torch.cuda.synchronize()
         if dist:
             dist.barrier()
         w0 = time.perf_counter()
@@ -345,34 +399,15 @@ def main():
         s1 = torch.cuda.Event(enable_timing=True)
         s0.record(stream)
         cp.wait_stream(stream)
-        with torch.cuda.stream(cp):
-            stage_in.copy_(host_in, non_blocking=True)
-        in_ready = ev()
-        in_ready.record(cp)
-        d2h_done = None
+        sim.upload_async(host_in.data_ptr(), cp)
         for k in range(a.steps):
-            stream.wait_event(in_ready)
-            sim.upload_device(stage_in.data_ptr(), stream)
-            consumed = ev()
-            consumed.record(stream)
+            sim.commit_upload(stream)
             if k + 1 < a.steps:
-                cp.wait_event(consumed)
-                with torch.cuda.stream(cp):
-                    stage_in.copy_(host_in, non_blocking=True)
-                in_ready = ev()
-                in_ready.record(cp)
+                sim.upload_async(host_in.data_ptr(), cp)
             one_step(False)
-            if d2h_done is not None:
-                stream.wait_event(d2h_done)
-            sim.download_device(stage_out.data_ptr(), stream)
-            out_ready = ev()
-            out_ready.record(stream)
-            cp.wait_event(out_ready)
-            with torch.cuda.stream(cp):
-                host_out.copy_(stage_out, non_blocking=True)
-            d2h_done = ev()
-            d2h_done.record(cp)
-        stream.wait_event(d2h_done)
+            sim.snapshot(stream)
+            sim.download_async(host_out.data_ptr(), cp)
+        stream.wait_stream(cp)
         s1.record(stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - w0
@@ -384,16 +419,19 @@ def main():
         nbytes = words * 4
         e2e = {"value": updates_per_step * a.steps / (e_ms / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": nbytes * world, "d2h_bytes_per_step": nbytes * world + 8 * 8,
+               "path": "kk_upload_packed_async / kk_commit_upload / kk_snapshot / kk_download_packed_async "
+                       "(C ABI) + the observables read back every step",
                "note": "per step: pinned-host->HBM upload of the step's input lattice (copy stream, overlapped "
                        "with the previous step), S sweeps + observables, lattice download (overlapped with "
                        "the next step); the last download is inside the timed region"}
 
+    out = None
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u1", "data": "synthetic",
-            "config": {"workload": f"configs[4]: {Lx}x{rows} slab per GPU (global {Lx}x{Ly}), "
+            "scaling": scaling, "vs_baseline": None, "dtype": "u1", "data": "synthetic",
+            "config": {"workload": f"configs[4]: {Lx}x{rows} slab per GPU (global {Lx}x{Ly}, {scaling} scaling), "
                                    f"{a.sweeps_per_step} sweeps + observables"
                                    + ("" if a.no_ccl else " + cluster histogram") + " per step",
                        "omega_kT": a.omega, "fraction_A": a.fraction, "start": "random",
@@ -408,14 +446,9 @@ def main():
             "e2e": e2e,
             "observables": obs,
         }
-        if world == 1 and not a.no_cpu_baseline:
-            out["cpu_baseline"] = cpu_baseline(a.cpu_seconds, a.omega, a.fraction, a.seed)
-        if world == 1 and not a.no_other_configs:
-            out["other_configs"] = other_configs(torch)
-        print(json.dumps(out), flush=True)
     sim.close()
-    if dist:
-        dist.destroy_process_group()
+    torch.cuda.synchronize()
+    return out
 
 
 if __name__ == "__main__":

@@ -189,6 +189,28 @@ int kk_set_lattice_packed(kk_handle h, const uint32_t* in, void* stream);
 int kk_copy_lattice_packed_device(kk_handle h, uint32_t* dst, int to_device_buffer,
                                   const uint32_t* src, void* stream);
 
+/* Double-buffered host I/O (GPU architecture: "copy whole data
+ * to device memory, then perform simulations and move it back"), for a
+ * pipeline whose copies overlap the sweeps.  The handle owns two device
+ * staging buffers (allocated on first use, one lattice each); every call is
+ * stream-ordered and returns without synchronising:
+ *   kk_upload_packed_async(h, host, copy_stream):  host -> staging-in
+ *     (waits, on copy_stream, until the previous upload was committed);
+ *   kk_commit_upload(h, stream):  staging-in -> the lattice, on `stream`
+ *     (waits for the upload's copy);
+ *   kk_snapshot(h, stream):  the lattice -> staging-out, on `stream` (waits
+ *     until the previous download has drained the staging buffer);
+ *   kk_download_packed_async(h, host, copy_stream):  staging-out -> host
+ *     (waits for the snapshot).
+ * host: uint32[replicas][y_count][W] in the packed layout above; pinned
+ * (cudaHostAlloc / cudaHostRegister) memory makes the copies asynchronous.
+ * The caller synchronises copy_stream before reading a download's host
+ * buffer or rewriting an upload's. */
+int kk_upload_packed_async(kk_handle h, const uint32_t* host, void* copy_stream);
+int kk_commit_upload(kk_handle h, void* stream);
+int kk_snapshot(kk_handle h, void* stream);
+int kk_download_packed_async(kk_handle h, uint32_t* host, void* copy_stream);
+
 /* Random start for slab handles (R7), which need a selection over ALL slabs:
  * create with KK_INIT_EMPTY, then
  *   for level 0,1,2: kk_init_select_hist(level, prefix) -> hist (host,
@@ -208,6 +230,26 @@ int kk_init_select_hist(kk_handle h, int level, const uint32_t* prefix, int64_t*
 int kk_init_select_ties(kk_handle h, const uint32_t* K, int64_t* out, int64_t capacity, int64_t* n_out,
                         void* stream);
 int kk_init_select_apply(kk_handle h, const uint32_t* K, const int64_t* cut, void* stream);
+
+/* The host steps between those calls (no handle, no GPU):
+ * kk_init_select_choose: one radix-select level over the slab-summed
+ *   histogram hist[replicas][2048] (level 2 uses bins 0..1023): per replica
+ *   the smallest bin whose cumulative count reaches need[r]; need[r] becomes
+ *   the rank inside that bin and prefix[r] = prefix[r] << 11 | bin (<< 10 at
+ *   level 2).  need, prefix: in/out host arrays of `replicas` entries.
+ * kk_init_select_cut: from the gathered ties (n_ties (replica, global
+ *   row-major index) pairs, any order) and the remaining need per replica,
+ *   cut[r] = the (need[r])-th smallest tie index of replica r, + 1 (0 if
+ *   need[r] == 0).  KK_ERR_STATE if a replica has fewer ties than need. */
+int kk_init_select_choose(int level, const int64_t* hist, int64_t replicas, int64_t* need, uint32_t* prefix);
+int kk_init_select_cut(const int64_t* ties, int64_t n_ties, int64_t replicas, const int64_t* need, int64_t* cut);
+
+/* Cluster-size histogram merge (host, R9): n (size, count) int64 pairs in any
+ * order (e.g. the slab-local rows of every rank and kk_cluster_join's rows)
+ * -> out: the histogram sorted by size with equal sizes summed, zero counts
+ * dropped.  *n_out = rows written; KK_ERR_CAPACITY (and the size needed) if
+ * out holds fewer than that many pairs. */
+int kk_hist_merge(const int64_t* rows, int64_t n, int64_t* out, int64_t capacity, int64_t* n_out);
 
 /* Acceptance thresholds actually used (R5): out[v+3], v = dN_AB/2 in -3..3,
  * accept iff u32 <= out[v+3] (and the pair is unlike). Host, 7 entries. */

@@ -42,10 +42,7 @@ cudaError_t ensure_dynamic_smem(const void* fn, int bytes) {
 int pass_smem_bytes(int T, int THI, int TWI);
 void set_pass_layout(int T, PassParams& P);
 void set_resident_layout(ResParams& P);
-int band_smem_bytes(const Geom& g, int nbands);
 void set_band_layout(BandParams& P);
-int64_t band_xch_words(const Geom& g, int nbands);
-cudaError_t launch_band(const BandParams& P, cudaStream_t stream);
 int cluster_smem_bytes(const Geom& g, int csize);
 cudaError_t launch_band_cluster(const BandParams& P, int64_t replicas, cudaStream_t stream);
 int cluster_tb_smem_bytes(const Geom& g, int csize, int TB);
@@ -123,7 +120,7 @@ struct kk_lattice {
     int nbands = 0;                   // > 0: kk_sweep runs the band kernel (lattice resident across all SMs)
     int cluster_size = 0;             // > 0: kk_sweep runs the cluster kernel (one cluster per replica)
     int cluster_tb = 1;               // its iterations per halo exchange (1: band_kernel<256, true>)
-    int band_tb = 1;                  // band kernel iterations per L2 halo exchange (1: band_kernel<1024, false>)
+    int band_tb = 1;                  // band kernel iterations per L2 halo exchange (2, 4 or 8)
     uint32_t* xch = nullptr;          // band kernel exchange rows
     unsigned int* band_flags = nullptr;
     unsigned int* band_error = nullptr;
@@ -146,6 +143,10 @@ struct kk_lattice {
     unsigned long long* row_off = nullptr;  // [R+1] their exclusive scan
     unsigned long long* rows_buf = nullptr; // compact dense rows (size << 32 | count)
     int64_t rows_cap = 0;
+    // double-buffered host I/O (lazy)
+    uint32_t* stage_in = nullptr;
+    uint32_t* stage_out = nullptr;
+    cudaEvent_t ev_in_ready = nullptr, ev_in_free = nullptr, ev_out_ready = nullptr, ev_out_free = nullptr;
 };
 
 namespace {
@@ -309,8 +310,11 @@ void set_slab_bands(kk_lattice* h) {
 // widths are whole 128-site groups).  Cost model per CTA: the item rounds of
 // the T iterations (interior rows + the light cone, ~1.5 rows per remaining
 // iteration on each side, R8; items = centre rows x (groups + 2 halo
-// groups); a round = pass_nt items) plus staging and a fixed cost; the grid
-// runs in waves of one CTA per SM.  KK_TWI / KK_THI force the targets.
+// groups); a round = pass_nt items, ~4 us on B200) plus staging and a fixed
+// cost; the grid runs in waves of one CTA per SM.  Measured on 65536^2
+// (tools/planar_tune.py): 128 x 356 609 G/s, 128 x 276 598, 128 x 200 577,
+// 64 x 596 578, 64 x 444 553, 32 x 996 529 — wide tiles (fewer halo groups)
+// and tall ones (fewer waves) both pay.  KK_TWI / KK_THI force the targets.
 void choose_tiles_planar(kk_lattice* h, int nsm) {
     const int T = h->T, NT = h->pass_nt;
     const int twi_env = env_int("KK_TWI", 0), thi_env = env_int("KK_THI", 0);
@@ -332,7 +336,7 @@ void choose_tiles_planar(kk_lattice* h, int nsm) {
     }
     double best = 1e300;
     int bt = 64, bh = 596;
-    for (int twi : {16, 32, 64, 128}) {
+    for (int twi : {128, 64, 32, 16}) {  // ties go to the widest tile (fewest halo groups)
         for (int thi = 8; thi <= 2048; thi += 4) {
             set_planar(twi, thi);
             if (planar_layout(T, h->THI, h->TWI, NT, nullptr) > 227 * 1024) break;
@@ -342,7 +346,7 @@ void choose_tiles_planar(kk_lattice* h, int nsm) {
                 const double rows = (h->THI + 3.0 * (T - 1 - t) + 2.0) / 4.0;
                 work += std::ceil(std::ceil(rows) * NG / NT);
             }
-            work += 0.25 * (double)(h->THI + 6 * T) * NG / NT + 2.0;  // staging + fixed
+            work += 0.05 * (double)(h->THI + 6 * T) * NG / NT + 1.0;  // staging (TMA) + fixed
             const int64_t ctas = (int64_t)h->tiles_x * h->bands * h->R;
             const double t = (double)((ctas + nsm - 1) / nsm) * work;
             if (t < best * 0.999) {
@@ -494,6 +498,10 @@ void free_all(kk_lattice* h) {
     cudaFree(h->xch);
     cudaFree(h->band_flags);
     cudaFree(h->band_error);
+    cudaFree(h->stage_in);
+    cudaFree(h->stage_out);
+    for (cudaEvent_t e : {h->ev_in_ready, h->ev_in_free, h->ev_out_ready, h->ev_out_free})
+        if (e) cudaEventDestroy(e);
 }
 
 // ---- exact-composition random start (R7): radix select in three steps.
@@ -587,6 +595,11 @@ void select_choose(int level, const int64_t* hist, int64_t R, int64_t* need, uin
     }
 }
 
+}  // namespace
+extern "C" int kk_init_select_cut(const int64_t* ties, int64_t n_ties, int64_t replicas, const int64_t* need,
+                                  int64_t* cut);
+namespace {
+
 int init_random_full(kk_lattice* h, cudaStream_t s) {
     const int64_t R = h->R;
     const int64_t nA = count_a_for(h->g.Lx * h->g.Ly, h->fraction_A);
@@ -604,14 +617,9 @@ int init_random_full(kk_lattice* h, cudaStream_t s) {
     int64_t n_out = 0;
     int rc = select_ties(h, prefix.data(), ties.data(), ntie, &n_out, s);
     if (rc != KK_OK) return rc;
-    std::vector<std::vector<int64_t>> per(R);
-    for (int64_t t = 0; t < n_out; ++t) per[ties[2 * t]].push_back(ties[2 * t + 1]);
     std::vector<int64_t> cut(R, 0);
-    for (int64_t r = 0; r < R; ++r) {
-        std::sort(per[r].begin(), per[r].end());
-        if (need[r] > (int64_t)per[r].size()) return fail(KK_ERR_STATE, "init: tie count mismatch");
-        cut[r] = need[r] > 0 ? per[r][need[r] - 1] + 1 : 0;
-    }
+    rc = kk_init_select_cut(ties.data(), n_out, R, need.data(), cut.data());
+    if (rc != KK_OK) return rc;
     return select_apply(h, prefix.data(), cut.data(), s);
 }
 
@@ -720,14 +728,31 @@ int plan_handle(kk_lattice* h, const kk_config* c, int T, int nsm) {
     // it beats the tile kernel from ~8192^2 until the bands no longer fit in
     // shared memory (8192^2: 330 -> 351 G/s, 12288^2: 400 -> 418;
     // tools/band_tb.py), so that range uses it by default (KK_BAND=0 off).
+    // planar tile kernel (kk_planar.cu): rows of whole 128-site groups
+    // (Lx % 128 == 0) and enough 32-centre items to fill the GPU (from
+    // 4096^2: 1024^2 23 vs 40 G/s, 2048^2 85 vs 121, 4096^2 294 vs 247,
+    // 8192^2 472 vs 351 on the band kernel, 65536^2 657 vs 490;
+    // tools/planar_rate.py).  KK_PLANAR=0 never, =2 whenever the rows allow.
+    const int pmode = env_int("KK_PLANAR", 1);
+    const bool planar_ok = pmode != 0 && !h->resident && h->g.tail == 0 && h->g.W % 4 == 0 &&
+                           (pmode == 2 || h->g.Lx * h->g.rows * h->R >= ((int64_t)1 << 24));
+    // band kernel (L2 halo exchange every TB = 4 iterations, 3*TB-row halos):
+    // KK_BAND=2 forces it where the bands fit (TB = 4, else 2); automatic only
+    // where the planar kernel does not apply (Lx % 128 != 0, >= 8192^2)
     const int bmode = env_int("KK_BAND", -1);
     const int nb = (int)std::min<int64_t>(nsm, h->g.rows / 4);
-    const bool band_auto = bmode < 0 && h->g.rows >= 48 * (int64_t)nb && h->g.Lx >= 8192 &&
+    const bool band_auto = bmode < 0 && !planar_ok && h->g.rows >= 48 * (int64_t)nb && h->g.Lx >= 8192 &&
                            band_tb_smem_bytes(h->g, nb, 4) > 0;
-    h->nbands = (!h->resident && h->R == 1 && (bmode == 2 || band_auto) && band_smem_bytes(h->g, nb) > 0) ? nb : 0;
-    {
-        const int tb = env_int("KK_BAND_TB", band_auto ? 4 : 1);
-        h->band_tb = (h->nbands && tb > 1 && band_tb_smem_bytes(h->g, nb, tb) > 0) ? tb : 1;
+    h->nbands = 0;
+    h->band_tb = 1;
+    if (!h->resident && h->R == 1 && (bmode == 2 || band_auto)) {
+        const int forced = env_int("KK_BAND_TB", 0);
+        for (int tb : {forced, 4, 2})
+            if ((tb == 2 || tb == 4 || tb == 8) && band_tb_smem_bytes(h->g, nb, tb) > 0) {
+                h->nbands = nb;
+                h->band_tb = tb;
+                break;
+            }
     }
     // cluster kernel: one thread-block cluster per replica, one row band per
     // CTA, halos over DSMEM every few iterations.  Auto (KK_CLUSTER unset) for
@@ -777,10 +802,7 @@ int plan_handle(kk_lattice* h, const kk_config* c, int T, int nsm) {
         h->resident = 0;
         h->nbands = 0;
     }
-    // planar tile kernel (kk_planar.cu): rows of whole 128-site groups
-    // (Lx % 128 == 0); KK_PLANAR=0 keeps the row-major tile kernel.
-    h->planar = !h->cluster_size && !h->nbands && !h->resident && h->g.tail == 0 && h->g.W % 4 == 0 &&
-                env_int("KK_PLANAR", 1) != 0;
+    h->planar = planar_ok && !h->cluster_size && !h->nbands;
     if (h->planar) {
         const int forced = env_int("KK_PASS_THREADS", 0);
         h->pass_nt = (forced == 512 || forced == 640 || forced == 768 || forced == 896) ? forced : 640;
@@ -853,7 +875,7 @@ int kk_plan_config(const kk_config* c, int n_sm, kk_plan* out) {
         out->ctas = tmp.R;
     } else if (out->kernel == KK_KERNEL_BAND) {
         out->threads = 1024;
-        out->smem_bytes = band_smem_bytes(tmp.g, tmp.nbands);
+        out->smem_bytes = band_tb_smem_bytes(tmp.g, tmp.nbands, tmp.band_tb);
         out->ctas = tmp.nbands;
     } else {
         out->threads = 256;
@@ -902,8 +924,7 @@ int kk_create_ex(kk_handle* out, const kk_config* c) {
     cudaError_t e3 = cudaMalloc(&h->stats, sizeof(unsigned long long) * 4 * h->R);
     cudaError_t e4 = cudaMalloc(&h->obs, sizeof(unsigned long long) * 2 * h->R);
     if (h->nbands && !e4) {
-        e4 = cudaMalloc(&h->xch, 4 * std::max(band_xch_words(h->g, h->nbands),
-                                              band_tb_xch_words(h->g, h->nbands, h->band_tb)));
+        e4 = cudaMalloc(&h->xch, 4 * band_tb_xch_words(h->g, h->nbands, h->band_tb));
         if (!e4) e4 = cudaMalloc(&h->band_flags, sizeof(unsigned int) * h->nbands);
         if (!e4) e4 = cudaMalloc(&h->band_error, sizeof(unsigned int));
         if (!e4) e4 = cudaMemset(h->band_error, 0, sizeof(unsigned int));
@@ -1032,13 +1053,8 @@ int kk_sweep(kk_handle h, int64_t n, void* stream) {
         B.xch = h->xch;
         B.flags = h->band_flags;
         B.error = h->band_error;
-        if (h->band_tb > 1) {
-            set_cluster_tb_layout(B, h->band_tb);
-            KK_CUDA(launch_band_tb(B, h->band_tb, S(stream)));
-        } else {
-            set_band_layout(B);
-            KK_CUDA(launch_band(B, S(stream)));
-        }
+        set_cluster_tb_layout(B, h->band_tb);
+        KK_CUDA(launch_band_tb(B, h->band_tb, S(stream)));
         h->cur ^= 1;
         h->sweep += n;
         return KK_OK;
@@ -1458,6 +1474,135 @@ int kk_halo_rows(kk_handle h, int64_t* rows) {
 int kk_sweep_index(kk_handle h, int64_t* s) {
     if (!h || !s) return fail(KK_ERR_ARG, "null argument");
     *s = h->sweep;
+    return KK_OK;
+}
+
+
+// ---- double-buffered host I/O ---------------------------------------------------
+}  // extern "C"
+
+namespace {
+
+int ensure_staging(kk_lattice* h) {
+    if (h->stage_in) return KK_OK;
+    const size_t bytes = (size_t)h->R * h->g.rep_words * 4;
+    if (cudaMalloc(&h->stage_in, bytes) || cudaMalloc(&h->stage_out, bytes) ||
+        cudaEventCreateWithFlags(&h->ev_in_ready, cudaEventDisableTiming) ||
+        cudaEventCreateWithFlags(&h->ev_in_free, cudaEventDisableTiming) ||
+        cudaEventCreateWithFlags(&h->ev_out_ready, cudaEventDisableTiming) ||
+        cudaEventCreateWithFlags(&h->ev_out_free, cudaEventDisableTiming)) {
+        cudaGetLastError();
+        cudaFree(h->stage_in);
+        cudaFree(h->stage_out);
+        h->stage_in = h->stage_out = nullptr;
+        return fail(KK_ERR_NOMEM, "staging buffers: device allocation failed");
+    }
+    // nothing in flight yet: the "free" events start completed
+    cudaEventRecord(h->ev_in_free, nullptr);
+    cudaEventRecord(h->ev_out_free, nullptr);
+    return KK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int kk_upload_packed_async(kk_handle h, const uint32_t* host, void* copy_stream) {
+    KK_CHECK_HANDLE(h);
+    if (!host) return fail(KK_ERR_ARG, "host is null");
+    int rc = ensure_staging(h);
+    if (rc != KK_OK) return rc;
+    cudaStream_t s = S(copy_stream);
+    const size_t bytes = (size_t)h->R * h->g.rep_words * 4;
+    KK_CUDA(cudaStreamWaitEvent(s, h->ev_in_free, 0));  // the previous upload has been committed
+    KK_CUDA(cudaMemcpyAsync(h->stage_in, host, bytes, cudaMemcpyHostToDevice, s));
+    KK_CUDA(cudaEventRecord(h->ev_in_ready, s));
+    return KK_OK;
+}
+
+int kk_commit_upload(kk_handle h, void* stream) {
+    KK_CHECK_HANDLE(h);
+    if (!h->stage_in) return fail(KK_ERR_STATE, "kk_commit_upload: no upload in flight");
+    cudaStream_t s = S(stream);
+    const size_t bytes = (size_t)h->R * h->g.rep_words * 4;
+    KK_CUDA(cudaStreamWaitEvent(s, h->ev_in_ready, 0));
+    h->lay_planar = false;  // the whole lattice is rewritten in the public layout
+    KK_CUDA(cudaMemcpyAsync(h->buf[h->cur], h->stage_in, bytes, cudaMemcpyDeviceToDevice, s));
+    KK_CUDA(cudaEventRecord(h->ev_in_free, s));
+    return KK_OK;
+}
+
+int kk_snapshot(kk_handle h, void* stream) {
+    KK_CHECK_HANDLE(h);
+    int rc = ensure_staging(h);
+    if (rc != KK_OK) return rc;
+    cudaStream_t s = S(stream);
+    rc = ensure_layout(h, false, s);
+    if (rc != KK_OK) return rc;
+    const size_t bytes = (size_t)h->R * h->g.rep_words * 4;
+    KK_CUDA(cudaStreamWaitEvent(s, h->ev_out_free, 0));  // the previous download has drained stage_out
+    KK_CUDA(cudaMemcpyAsync(h->stage_out, h->buf[h->cur], bytes, cudaMemcpyDeviceToDevice, s));
+    KK_CUDA(cudaEventRecord(h->ev_out_ready, s));
+    return KK_OK;
+}
+
+int kk_download_packed_async(kk_handle h, uint32_t* host, void* copy_stream) {
+    KK_CHECK_HANDLE(h);
+    if (!host) return fail(KK_ERR_ARG, "host is null");
+    if (!h->stage_out) return fail(KK_ERR_STATE, "kk_download_packed_async: no snapshot");
+    cudaStream_t s = S(copy_stream);
+    const size_t bytes = (size_t)h->R * h->g.rep_words * 4;
+    KK_CUDA(cudaStreamWaitEvent(s, h->ev_out_ready, 0));
+    KK_CUDA(cudaMemcpyAsync(host, h->stage_out, bytes, cudaMemcpyDeviceToHost, s));
+    KK_CUDA(cudaEventRecord(h->ev_out_free, s));
+    return KK_OK;
+}
+
+// ---- host steps of the distributed random start and of the histogram merge --------
+int kk_init_select_choose(int level, const int64_t* hist, int64_t replicas, int64_t* need, uint32_t* prefix) {
+    if (level < 0 || level > 2 || !hist || !need || !prefix || replicas < 1)
+        return fail(KK_ERR_ARG, "kk_init_select_choose: bad argument");
+    select_choose(level, hist, replicas, need, prefix);
+    return KK_OK;
+}
+
+int kk_init_select_cut(const int64_t* ties, int64_t n_ties, int64_t replicas, const int64_t* need, int64_t* cut) {
+    if ((!ties && n_ties > 0) || n_ties < 0 || !need || !cut || replicas < 1)
+        return fail(KK_ERR_ARG, "kk_init_select_cut: bad argument");
+    std::vector<std::vector<int64_t>> per((size_t)replicas);
+    for (int64_t t = 0; t < n_ties; ++t) {
+        const int64_t r = ties[2 * t];
+        if (r < 0 || r >= replicas) return fail(KK_ERR_ARG, "kk_init_select_cut: replica index out of range");
+        per[(size_t)r].push_back(ties[2 * t + 1]);
+    }
+    for (int64_t r = 0; r < replicas; ++r) {
+        auto& v = per[(size_t)r];
+        if (need[r] < 0 || need[r] > (int64_t)v.size()) return fail(KK_ERR_STATE, "init: tie count mismatch");
+        if (need[r] == 0) {
+            cut[r] = 0;
+            continue;
+        }
+        std::nth_element(v.begin(), v.begin() + (need[r] - 1), v.end());
+        cut[r] = v[(size_t)need[r] - 1] + 1;
+    }
+    return KK_OK;
+}
+
+int kk_hist_merge(const int64_t* rows, int64_t n, int64_t* out, int64_t capacity, int64_t* n_out) {
+    if ((!rows && n > 0) || n < 0 || !n_out) return fail(KK_ERR_ARG, "kk_hist_merge: bad argument");
+    std::map<int64_t, int64_t> m;
+    for (int64_t k = 0; k < n; ++k) m[rows[2 * k]] += rows[2 * k + 1];
+    int64_t cnt = 0;
+    for (const auto& kv : m) cnt += kv.second != 0;
+    *n_out = cnt;
+    if (cnt > capacity || (!out && cnt > 0)) return fail(KK_ERR_CAPACITY, "histogram buffer too small");
+    int64_t i = 0;
+    for (const auto& kv : m)
+        if (kv.second != 0) {
+            out[2 * i] = kv.first;
+            out[2 * i + 1] = kv.second;
+            ++i;
+        }
     return KK_OK;
 }
 

@@ -19,10 +19,9 @@
 //  * resident_kernel<NT>: replicas that fit in one SM's shared memory; one
 //    CTA per replica runs every iteration of a kk_sweep call in place, the
 //    periodic wrap kept as rebuilt copies.
-//  * band_kernel<NT, CLU>: one row band per CTA, the whole lattice in shared
-//    memory for all iterations of a call, 3-row halos exchanged per
-//    iteration — across all SMs through L2 with release/acquire flags
-//    (opt-in), or inside one thread-block cluster per replica through DSMEM.
+//  * band_kernel<NT>: one row band per CTA of a thread-block cluster, the
+//    whole replica in shared memory for all iterations of a call, 3-row halos
+//    pushed over DSMEM after every iteration (KK_CLUSTER_TB=1).
 //  * cluster_kernel<NT, TB>: the cluster variant with 3*TB-row halos pushed
 //    over DSMEM once every TB iterations (default for single or few
 //    mid-small lattices).
@@ -810,17 +809,15 @@ __global__ void __launch_bounds__(NT, 1024 / NT) resident_kernel(const ResParams
 }
 
 
-// ---- band kernel -----------------------------------------------------------------
-// Mid-size lattices (too big for one SM, too small to fill the GPU with tiles
-// without heavy halo recomputation, e.g. 4096^2): the lattice is cut into
-// `nbands` row bands, one co-resident CTA each (cooperative launch), and stays
-// in shared memory for every iteration of a kk_sweep call.  After each
-// iteration a band publishes its first and last 3 rows to an L2 exchange
-// buffer, raises its flag (release), waits for both neighbours' flags
-// (acquire) and copies their rows into its 3-row halos.  Centres in the rows
-// just outside the band are processed redundantly by both neighbours (same
-// draws, same inputs: R8 with T = 1), so no flip ever crosses a band; flips
-// that land in a halo row are simply overwritten by the next exchange.
+// ---- band kernel (cluster variant) ----------------------------------------------
+// One row band per CTA of a thread-block cluster (one cluster per replica),
+// the whole replica in shared memory for every iteration of a kk_sweep call;
+// after each iteration the 3-row halos are pushed into the neighbours' shared
+// memory (DSMEM) and one cluster barrier orders them.  Centres in the rows just
+// outside the band are processed redundantly by both neighbours (same draws,
+// same inputs: R8 with T = 1), so no flip ever crosses a band; flips that land
+// in a halo row are overwritten by the next exchange.  KK_CLUSTER_TB=1 selects
+// it; the default cluster path is cluster_kernel (halos every TB iterations).
 // Shared layout as the resident kernel's, with local row lr = y - y0 + 3.
 
 __device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p) {
@@ -882,15 +879,11 @@ __device__ __forceinline__ void class_rows(int ky, int lo, int hi, int& first, i
     n = hi > first ? (hi - first + 3) / 4 : 0;
 }
 
-// CLU: the bands of one replica form a thread-block cluster (nbands = cluster
-// size, one cluster per replica) and the 3-row halos are read straight from
-// the neighbouring CTAs' shared memory (DSMEM) between two cluster barriers,
-// instead of the L2 exchange buffer and flags.
-template <int NT, bool CLU>
+template <int NT>
 __global__ void __launch_bounds__(NT, 1) band_kernel(const BandParams P) {
     const int nb = P.nbands;
-    const int b = CLU ? (int)(blockIdx.x % (unsigned)nb) : (int)blockIdx.x;
-    const int rep = CLU ? (int)(blockIdx.x / (unsigned)nb) : 0;
+    const int b = (int)(blockIdx.x % (unsigned)nb);
+    const int rep = (int)(blockIdx.x / (unsigned)nb);
     const Geom& g = P.g;
     const uint32_t* src_rep = P.src + (int64_t)rep * g.rep_words;
     const int W = g.W, tail = g.tail;
@@ -970,81 +963,40 @@ __global__ void __launch_bounds__(NT, 1) band_kernel(const BandParams P) {
         default: band_iteration<3, NT>(S, wk, R1, N1, R2, N2, sweep, c3, P.rk, acc); break;          \
     }
             KK_BAND_ITEMS(rt, nt_, rb, nb_)
-            if constexpr (CLU) {
-                namespace cg = cooperative_groups;
-                cg::cluster_group cl = cg::this_cluster();
-                __syncthreads();  // my first and last 3 own rows are final for this iteration
-                // push them into the neighbours' halo buffers of the next
-                // parity (they read the other parity meanwhile): up gets my
-                // first 3 rows as its bottom halo, dn my last 3 as its top halo
-                ++gi;
-                const int par = (int)(gi & 1u);
-                uint32_t* bu = cl.map_shared_rank(kk_smem + P.xbuf_off + par * 6 * W, up);
-                uint32_t* bd = cl.map_shared_rank(kk_smem + P.xbuf_off + par * 6 * W, dn);
-                for (int i = threadIdx.x; i < 6 * W; i += NT) {
-                    const int k6 = i / W, x = i - k6 * W;
-                    if (k6 < 3) bd[k6 * W + x] = kk_smem[(BR + k6) * WS + kCol0 + 1 + x];
-                    else bu[k6 * W + x] = kk_smem[k6 * WS + kCol0 + 1 + x];  // own rows 3..5
-                }
-                KK_BAND_ITEMS(ri, ni, 0, 0)
-                acc_flush(acc);
-                cl.sync();  // every push and every flip of this iteration has landed
-                // halo rows (all words, x copies included) from the buffer, and
-                // the x copies of the own rows, in one pass
-                const int xb = P.xbuf_off + par * 6 * W;
-                const int nx = tail ? 3 : 2;
-                const int n_halo = 6 * (W + 2), n_own = BR * nx;
-                for (int i = threadIdx.x; i < n_halo + n_own; i += NT) {
-                    if (i < n_halo) {
-                        const int k6 = i / (W + 2), w = i - k6 * (W + 2);
-                        const int lr = k6 < 3 ? k6 : BR + k6;  // 0..2, BR+3..BR+5
-                        kk_smem[lr * WS + kCol0 + w] = res_word(xb + k6 * W - 1, w, W, tail);
-                    } else {
-                        const int i2 = i - n_halo, a = i2 / nx, k = i2 - a * nx;
-                        const int lr = 3 + a, w = k == 0 ? 0 : (k == 1 ? W + 1 : W);
-                        kk_smem[lr * WS + kCol0 + w] = res_word(lr * WS + kCol0, w, W, tail);
-                    }
-                }
-                __syncthreads();
-                continue;
-            }
-            __syncthreads();
-            // publish: side 0 = first 3 real rows, side 1 = last 3
+            namespace cg = cooperative_groups;
+            cg::cluster_group cl = cg::this_cluster();
+            __syncthreads();  // my first and last 3 own rows are final for this iteration
+            // push them into the neighbours' halo buffers of the next
+            // parity (they read the other parity meanwhile): up gets my
+            // first 3 rows as its bottom halo, dn my last 3 as its top halo
             ++gi;
-            const int slot = (int)(gi & 1u);
-            uint32_t* xo = P.xch + (int64_t)b * xband + slot * xslot;
+            const int par = (int)(gi & 1u);
+            uint32_t* bu = cl.map_shared_rank(kk_smem + P.xbuf_off + par * 6 * W, up);
+            uint32_t* bd = cl.map_shared_rank(kk_smem + P.xbuf_off + par * 6 * W, dn);
             for (int i = threadIdx.x; i < 6 * W; i += NT) {
                 const int k6 = i / W, x = i - k6 * W;
-                const int lr = k6 < 3 ? 3 + k6 : BR + k6 - 3;
-                xo[(k6 < 3 ? 0 : xside) + (k6 % 3) * xrow + x] = kk_smem[lr * WS + kCol0 + 1 + x];
+                if (k6 < 3) bd[k6 * W + x] = kk_smem[(BR + k6) * WS + kCol0 + 1 + x];
+                else bu[k6 * W + x] = kk_smem[k6 * WS + kCol0 + 1 + x];  // own rows 3..5
             }
-            __syncthreads();
-            // the barrier orders the CTA's stores before thread 0's release
-            // (cumulative), which orders them before the flag
-            if (threadIdx.x == 0) st_release(P.flags + b, gi);
             KK_BAND_ITEMS(ri, ni, 0, 0)
             acc_flush(acc);
-            if (threadIdx.x == 0) {
-                long long spins = 0;
-                while (ld_acquire(P.flags + up) < gi || ld_acquire(P.flags + dn) < gi) {
-                    if (++spins > (1ll << 24)) {  // a neighbour never arrived (~1 s): give up loudly
-                        atomicExch(P.error, 1u);
-                        break;
-                    }
+            cl.sync();  // every push and every flip of this iteration has landed
+            // halo rows (all words, x copies included) from the buffer, and
+            // the x copies of the own rows, in one pass
+            const int xb = P.xbuf_off + par * 6 * W;
+            const int nx = tail ? 3 : 2;
+            const int n_halo = 6 * (W + 2), n_own = BR * nx;
+            for (int i = threadIdx.x; i < n_halo + n_own; i += NT) {
+                if (i < n_halo) {
+                    const int k6 = i / (W + 2), w = i - k6 * (W + 2);
+                    const int lr = k6 < 3 ? k6 : BR + k6;  // 0..2, BR+3..BR+5
+                    kk_smem[lr * WS + kCol0 + w] = res_word(xb + k6 * W - 1, w, W, tail);
+                } else {
+                    const int i2 = i - n_halo, a = i2 / nx, k = i2 - a * nx;
+                    const int lr = 3 + a, w = k == 0 ? 0 : (k == 1 ? W + 1 : W);
+                    kk_smem[lr * WS + kCol0 + w] = res_word(lr * WS + kCol0, w, W, tail);
                 }
             }
-            __syncthreads();
-            // halos: rows y0-3..y0-1 = up's last 3 rows, y1..y1+2 = dn's first 3 rows
-            const uint32_t* xu = P.xch + (int64_t)up * xband + slot * xslot + xside;
-            const uint32_t* xd = P.xch + (int64_t)dn * xband + slot * xslot;
-            for (int i = threadIdx.x; i < 6 * W; i += NT) {
-                const int k6 = i / W, x = i - k6 * W;
-                const int lr = k6 < 3 ? k6 : BR + k6;  // 0..2 and BR+3..BR+5
-                const uint32_t* src = k6 < 3 ? xu : xd;
-                kk_smem[lr * WS + kCol0 + 1 + x] = __ldcg(src + (k6 % 3) * xrow + x);
-            }
-            __syncthreads();
-            band_refresh<NT>(S, H);
             __syncthreads();
 #undef KK_BAND_ITEMS
         }
@@ -1482,9 +1434,10 @@ cudaError_t launch_resident(const ResParams& P, int64_t replicas, int nt, cudaSt
     return cudaGetLastError();
 }
 
-// Band kernel geometry: 1024-thread CTAs, one per SM; 0 if the lattice does
-// not qualify (full periodic lattice, one replica, Lx >= 64 and W >= 3 with a
-// tail, every band >= 4 rows and within shared memory).
+// Band geometry (cluster band kernel; 1024-thread CTAs for the L2 band kernel
+// with temporal blocking): 0 if the lattice does not qualify (full periodic
+// lattice, Lx >= 64 and W >= 3 with a tail, every band >= 4 rows and within
+// shared memory).
 constexpr int kBandThreads = 1024;
 
 int band_smem_bytes(const Geom& g, int nbands) {
@@ -1512,23 +1465,6 @@ void set_band_layout(BandParams& P) {
     P.xbuf_off = (L.words + 3) & ~3;
 }
 
-int64_t band_xch_words(const Geom& g, int nbands) { return (int64_t)nbands * 2 * 2 * 3 * g.W; }
-
-cudaError_t launch_band(const BandParams& P, cudaStream_t stream) {
-    const int smem = band_smem_bytes(P.g, P.nbands);
-    if (!smem) return cudaErrorInvalidValue;
-    cudaError_t e = ensure_dynamic_smem((const void*)band_kernel<kBandThreads, false>, smem);
-    if (e != cudaSuccess) return e;
-    e = cudaMemsetAsync(P.flags, 0, sizeof(unsigned int) * P.nbands, stream);
-    if (e != cudaSuccess) return e;
-    void* args[] = {const_cast<BandParams*>(&P)};
-    e = cudaLaunchCooperativeKernel((const void*)band_kernel<kBandThreads, false>, dim3((unsigned)P.nbands),
-                                    dim3(kBandThreads), args, (size_t)smem, stream);
-    if (e != cudaSuccess) return e;
-    count_launch();
-    return cudaGetLastError();
-}
-
 #ifdef KK_PASS_CLK
 extern "C" int kk_debug_pass_clocks(unsigned long long* out) {
     cudaMemcpyFromSymbol(out, kk_pass_clk, sizeof(kk_pass_clk));
@@ -1551,7 +1487,7 @@ int cluster_smem_bytes(const Geom& g, int csize) {
 cudaError_t launch_band_cluster(const BandParams& P, int64_t replicas, cudaStream_t stream) {
     const int smem = cluster_smem_bytes(P.g, P.nbands);
     if (!smem) return cudaErrorInvalidValue;
-    const void* fn = (const void*)band_kernel<kClusterThreads, true>;
+    const void* fn = (const void*)band_kernel<kClusterThreads>;
     cudaError_t e = ensure_dynamic_smem(fn, smem);
     if (e != cudaSuccess) return e;
     if (P.nbands > 8) {
@@ -1570,7 +1506,7 @@ cudaError_t launch_band_cluster(const BandParams& P, int64_t replicas, cudaStrea
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, band_kernel<kClusterThreads, true>, P);
+    e = cudaLaunchKernelEx(&cfg, band_kernel<kClusterThreads>, P);
     if (e != cudaSuccess) return e;
     count_launch();
     return cudaGetLastError();
@@ -1651,7 +1587,7 @@ int cluster_max_active(const Geom& g, int csize, int TB) {
     const void* fn = TB == 2   ? (const void*)cluster_kernel<kClusterThreads, 2, false>
                      : TB == 4 ? (const void*)cluster_kernel<kClusterThreads, 4, false>
                      : TB == 8 ? (const void*)cluster_kernel<kClusterThreads, 8, false>
-                               : (const void*)band_kernel<kClusterThreads, true>;
+                               : (const void*)band_kernel<kClusterThreads>;
     if (ensure_dynamic_smem(fn, smem) != cudaSuccess) {
         cudaGetLastError();
         return 0;

@@ -167,11 +167,11 @@ __device__ __forceinline__ void pl_iteration(const PlCtx& X, uint32_t* tile, con
         const bool has = base + (int)threadIdx.x < items;
         const int r = r_first + 4 * a;
         uint32_t need = 0, nontriv = 0, autoacc = 0, M0 = 0, M1 = 0, up = 0, dn = 0, D0 = 0, D1 = 0, D2 = 0;
-        uint32_t rlw = 0, drawn = 0;
+        uint32_t rlw = 0, drawn = 0, l = 0, Mg = 0;
         if (has) {
             rlw = rl[r];
-            const uint32_t l = rlw & 0x7FFFFFFFu;
-            const uint32_t Mg = gt[m];
+            l = rlw & 0x7FFFFFFFu;
+            Mg = gt[m];
             // ---- direction draws (R6): call 4g for octet g = 4 Mg + o, word k2 = pair k2
             uint32_t R4[4][4];
             {
@@ -262,11 +262,16 @@ __device__ __forceinline__ void pl_iteration(const PlCtx& X, uint32_t* tile, con
             dn = mux(C, ltm, gtm);  // v < 0
             need = nontriv & mux(X.mdn, dn, up) & X.mall;
             autoacc = nontriv & ~need;
-            // ---- acceptance draws (R6): call 4g + 1 + h holds the uniforms of
-            // quad k = 2 (g - 4 Mg) + h (centres 4k..4k+3); all eight calls of
-            // the item, in two batches of four interleaved streams.  Each
-            // uniform is tested against the thresholds of |v| = 1, 2, 3 (R5)
-            // and the centre's own |v| picks the result.
+        }
+        // ---- acceptance draws (R6): call 4g + 1 + h holds the uniforms of
+        // quad k = 2 (g - 4 Mg) + h (centres 4k..4k+3); all eight calls of the
+        // item, in two batches of four interleaved streams.  Each uniform is
+        // tested against the thresholds of |v| = 1, 2, 3 (R5) and the
+        // centre's own |v| picks the result; the |v| = 2 and 3 tests are
+        // skipped (warp-uniformly) when no centre of the warp needs them.
+        const bool any2 = __any_sync(0xFFFFFFFFu, need & M1 & ~M0);
+        const bool any3 = __any_sync(0xFFFFFFFFu, need & M1 & M0);
+        if (has) {
             uint32_t L1 = 0, L2 = 0, L3 = 0;
 #pragma unroll
             for (int bt = 0; bt < 2; ++bt) {
@@ -275,14 +280,20 @@ __device__ __forceinline__ void pl_iteration(const PlCtx& X, uint32_t* tile, con
                 uint32_t U[4][4];
                 philox10_xn<4>(mm, l, X.sweep, X.c3, X.rk, U);
 #pragma unroll
-                for (int qd = 0; qd < 4; ++qd) {
+                for (int qd = 0; qd < 4; ++qd)
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const uint32_t bit = 1u << (16 * bt + 4 * qd + i);
-                        L1 = or_if_le(L1, U[qd][i], X.t1, bit);
-                        L2 = or_if_le(L2, U[qd][i], X.t2, bit);
-                        L3 = or_if_le(L3, U[qd][i], X.t3, bit);
-                    }
+                    for (int i = 0; i < 4; ++i) L1 = or_if_le(L1, U[qd][i], X.t1, 1u << (16 * bt + 4 * qd + i));
+                if (any2) {
+#pragma unroll
+                    for (int qd = 0; qd < 4; ++qd)
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) L2 = or_if_le(L2, U[qd][i], X.t2, 1u << (16 * bt + 4 * qd + i));
+                }
+                if (any3) {
+#pragma unroll
+                    for (int qd = 0; qd < 4; ++qd)
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) L3 = or_if_le(L3, U[qd][i], X.t3, 1u << (16 * bt + 4 * qd + i));
                 }
             }
             drawn = need & mux(M1, mux(M0, L3, L2), L1);

@@ -181,36 +181,20 @@ class GpuSlab:
 
 
 # ------------------------------------------------------------- random start
-def select_choose(level: int, hist: np.ndarray, need: np.ndarray, prefix: np.ndarray):
-    """Host bin choice of one radix-select level (mirrors include/kk.h)."""
-    nbins = 1024 if level == 2 else 2048
-    for r in range(hist.shape[0]):
-        c = np.cumsum(hist[r, :nbins])
-        b = int(np.searchsorted(c, need[r], side="left"))
-        b = min(b, nbins - 1)
-        before = int(c[b - 1]) if b > 0 else 0
-        need[r] -= before
-        prefix[r] = (int(prefix[r]) << (10 if level == 2 else 11)) | b
-
-
 def distributed_random_init(lat, comm, fraction_A: float, Lx: int, Ly: int):
-    """Exact-composition random start (R7) over all slabs."""
+    """Exact-composition random start (R7) over all slabs: histograms summed
+    and ties gathered here; the bin choice and the tie cut are the library's
+    host steps (kk_init_select_choose / kk_init_select_cut)."""
     R = lat.replicas
     nA = int(np.floor(fraction_A * Lx * Ly + 0.5))
     need = np.full(R, nA, np.int64)
-    prefix = np.zeros(R, np.int64)
+    prefix = np.zeros(R, np.uint32)
     for level in range(3):
-        h = lat.select_hist(level, None if level == 0 else (prefix & 0xFFFFFFFF).astype(np.uint32))
+        h = lat.select_hist(level, None if level == 0 else prefix)
         h = comm.all_reduce_sum(h)
-        select_choose(level, h, need, prefix)
-    K = (prefix & 0xFFFFFFFF).astype(np.uint32)
-    ties = comm.all_gather_rows(lat.select_ties(K))
-    cut = np.zeros(R, np.int64)
-    for r in range(R):
-        idx = np.sort(ties[ties[:, 0] == r, 1])
-        assert need[r] <= idx.size, "tie count mismatch"
-        cut[r] = idx[need[r] - 1] + 1 if need[r] > 0 else 0
-    lat.select_apply(K, cut)
+        kk.select_choose(level, h, need, prefix)
+    ties = comm.all_gather_rows(lat.select_ties(prefix))
+    lat.select_apply(prefix, kk.select_cut(ties, R, need))
 
 
 # ------------------------------------------------------------------ driver
@@ -230,17 +214,31 @@ class SlabDriver:
             be.commit()
             return
         be.pack_halo(self.send_top, self.send_bot, self.stream)
-        works = self.comm.exchange_start(self.send_top, self.send_bot, self.recv_top, self.recv_bot)
+        with self._on_stream():
+            # NCCL orders its send after the current stream (the halo pack) and
+            # Work.wait() orders the current stream after the receive, so both
+            # happen with the driver's stream current: the boundary pass below
+            # runs on that stream
+            works = self.comm.exchange_start(self.send_top, self.send_bot, self.recv_top, self.recv_bot)
         if self.side is not None:
             self.side.wait_stream(self.stream)
             be.run_pass(kk.REGION_INTERIOR, None, None, self.side)
         else:
             be.run_pass(kk.REGION_INTERIOR, None, None, self.stream)
-        self.comm.exchange_wait(works)
+        with self._on_stream():
+            self.comm.exchange_wait(works)
         be.run_pass(kk.REGION_BOUNDARY, self.recv_top, self.recv_bot, self.stream)
         if self.side is not None:
             self.stream.wait_stream(self.side)
         be.commit()
+
+    def _on_stream(self):
+        """Context making the driver's CUDA stream current (no-op without one)."""
+        import contextlib
+        if self.stream is None or not hasattr(self.stream, "cuda_stream"):
+            return contextlib.nullcontext()
+        import torch
+        return torch.cuda.stream(self.stream)
 
     def sweep(self, n: int, T: int):
         for _ in range(n * (16 // T)):
@@ -249,8 +247,9 @@ class SlabDriver:
     def refresh_halos(self):
         if self.world > 1:
             self.be.pack_halo(self.send_top, self.send_bot, self.stream)
-            self.comm.exchange_wait(self.comm.exchange_start(self.send_top, self.send_bot,
-                                                             self.recv_top, self.recv_bot))
+            with self._on_stream():
+                self.comm.exchange_wait(self.comm.exchange_start(self.send_top, self.send_bot,
+                                                                 self.recv_top, self.recv_bot))
 
     def cluster_histogram(self, target: int = 1):
         """Cluster-size histogram [(size, count)] of the whole lattice (R9), on
@@ -275,10 +274,8 @@ class SlabDriver:
         sizes_all = torch.cat([sz[: int(n)] for sz, n in zip(sizes, ns)]) if int(ns.sum()) else sizes[0][:1]
         jrows = be.cluster_join(be.Lx, self.world, torch.cat(tops), torch.cat(bots), offsets, sizes_all,
                                 int(ns.sum()), self.stream)
-        hist = {}
-        for sz, c in list(map(tuple, all_rows.tolist())) + list(map(tuple, np.asarray(jrows).tolist())):
-            hist[sz] = hist.get(sz, 0) + c
-        return sorted(hist.items())
+        return kk.hist_merge(np.concatenate([np.asarray(all_rows, np.int64).reshape(-1, 2),
+                                             np.asarray(jrows, np.int64).reshape(-1, 2)]))
 
     def observe(self, ccl: bool = True) -> dict:
         """N_AB, composition and counters summed over slabs, and the cluster
@@ -322,6 +319,19 @@ class Simulation:
     def upload_packed(self, host_ptr: int):
         self.lat.set_packed_ptr(host_ptr, self.driver.stream)
 
+    # double-buffered host I/O through the C ABI (kk_upload_packed_async ...)
+    def upload_async(self, host_ptr: int, copy_stream):
+        self.lat.upload_async(host_ptr, copy_stream)
+
+    def commit_upload(self, stream=None):
+        self.lat.commit_upload(stream if stream is not None else self.driver.stream)
+
+    def snapshot(self, stream=None):
+        self.lat.snapshot(stream if stream is not None else self.driver.stream)
+
+    def download_async(self, host_ptr: int, copy_stream):
+        self.lat.download_async(host_ptr, copy_stream)
+
     def upload_device(self, dev_ptr: int, stream=None):
         """Lattice <- packed words at a device address (same layout)."""
         self.lat.copy_packed_device(dev_ptr, True, stream if stream is not None else self.driver.stream)
@@ -340,6 +350,15 @@ class Simulation:
         self.lat.close()
 
 
+def slab_rows(Ly: int, world: int) -> int:
+    """Rows per rank of a row-slab split: every rank holds the same number of
+    rows, a multiple of 4 (the centre classes, R10); anything else would leave
+    rows unsimulated or break the phase of the slabs below."""
+    if world < 1 or Ly % world != 0 or (Ly // world) % 4 != 0:
+        raise ValueError(f"Ly={Ly} does not split into {world} slabs of equal height divisible by 4")
+    return Ly // world
+
+
 def make_simulation(Lx: int, Ly: int, fraction_A: float, omega: float, seed: int, T: int = 4,
                     world: int = 1, rank: int = 0, device: int = 0, stream=None) -> Simulation:
     import torch
@@ -347,7 +366,7 @@ def make_simulation(Lx: int, Ly: int, fraction_A: float, omega: float, seed: int
         lat = kk.Lattice(Lx, Ly, fraction_A, omega, seed, iters_per_pass=T, device=device)
         drv = SlabDriver(GpuSlab(lat, torch.device("cuda", device)), None, 0, 1, stream)
         return Simulation(drv, lat, T)
-    rows = Ly // world
+    rows = slab_rows(Ly, world)
     lat = kk.Lattice(Lx, Ly, fraction_A, omega, seed, init=kk.KK_INIT_EMPTY, iters_per_pass=T,
                      y_begin=rank * rows, y_count=rows, device=device)
     comm = TorchComm(rank, world, torch.device("cuda", device))

@@ -76,6 +76,13 @@ SIGNATURES = {
     "kk_pack_halo": (ctypes.c_int, [_p, _p, _p, _p]),
     "kk_pass": (ctypes.c_int, [_p, ctypes.c_int, _p, _p, _p]),
     "kk_pass_commit": (ctypes.c_int, [_p]),
+    "kk_upload_packed_async": (ctypes.c_int, [_p, _p, _p]),
+    "kk_commit_upload": (ctypes.c_int, [_p, _p]),
+    "kk_snapshot": (ctypes.c_int, [_p, _p]),
+    "kk_download_packed_async": (ctypes.c_int, [_p, _p, _p]),
+    "kk_init_select_choose": (ctypes.c_int, [ctypes.c_int, _p, _i64, _p, _p]),
+    "kk_init_select_cut": (ctypes.c_int, [_p, _i64, _i64, _p, _p]),
+    "kk_hist_merge": (ctypes.c_int, [_p, _i64, _p, _i64, ctypes.POINTER(_i64)]),
     "kk_launch_count": (ctypes.c_int64, []),
     "kk_last_error": (ctypes.c_char_p, []),
     "kk_version": (ctypes.c_char_p, []),
@@ -133,6 +140,34 @@ def cluster_join(Lx: int, nslabs: int, top_ids: int, bot_ids: int, offsets, size
             continue
         _check(rc, "kk_cluster_join")
         return buf[: n.value]
+
+
+def select_choose(level: int, hist: np.ndarray, need: np.ndarray, prefix: np.ndarray):
+    """kk_init_select_choose: one radix-select level (need, prefix updated in place)."""
+    hist = np.ascontiguousarray(hist, np.int64)
+    assert need.dtype == np.int64 and prefix.dtype == np.uint32 and need.flags["C_CONTIGUOUS"]
+    _check(load().kk_init_select_choose(int(level), hist.ctypes.data, int(hist.shape[0]), need.ctypes.data,
+                                        prefix.ctypes.data), "kk_init_select_choose")
+
+
+def select_cut(ties: np.ndarray, replicas: int, need: np.ndarray) -> np.ndarray:
+    """kk_init_select_cut: per replica, index of the last tie taken + 1."""
+    ties = np.ascontiguousarray(ties, np.int64).reshape(-1, 2)
+    need = np.ascontiguousarray(need, np.int64)
+    cut = np.zeros(replicas, np.int64)
+    _check(load().kk_init_select_cut(ties.ctypes.data if len(ties) else None, len(ties), int(replicas),
+                                     need.ctypes.data, cut.ctypes.data), "kk_init_select_cut")
+    return cut
+
+
+def hist_merge(rows) -> list:
+    """kk_hist_merge: (size, count) pairs in any order -> sorted merged histogram."""
+    rows = np.ascontiguousarray(np.asarray(rows, np.int64).reshape(-1, 2))
+    out = np.zeros((max(len(rows), 1), 2), np.int64)
+    n = _i64()
+    _check(load().kk_hist_merge(rows.ctypes.data if len(rows) else None, len(rows), out.ctypes.data, len(out),
+                                ctypes.byref(n)), "kk_hist_merge")
+    return [tuple(r) for r in out[: n.value].tolist()]
 
 
 def plan(Lx: int, Ly: int, replicas: int = 1, iters_per_pass: int = 0, y_begin: int = 0,
@@ -355,6 +390,20 @@ class Lattice:
     def set_packed_ptr(self, host_ptr: int, stream=None):
         """Upload from a (pinned) host buffer given by address."""
         _check(load().kk_set_lattice_packed(self._h, host_ptr, stream_ptr(stream)), "kk_set_lattice_packed")
+
+    # -- double-buffered host I/O (include/kk.h kk_upload_packed_async ...)
+    def upload_async(self, host_ptr: int, copy_stream=None):
+        _check(load().kk_upload_packed_async(self._h, host_ptr, stream_ptr(copy_stream)), "kk_upload_packed_async")
+
+    def commit_upload(self, stream=None):
+        _check(load().kk_commit_upload(self._h, stream_ptr(stream)), "kk_commit_upload")
+
+    def snapshot(self, stream=None):
+        _check(load().kk_snapshot(self._h, stream_ptr(stream)), "kk_snapshot")
+
+    def download_async(self, host_ptr: int, copy_stream=None):
+        _check(load().kk_download_packed_async(self._h, host_ptr, stream_ptr(copy_stream)),
+               "kk_download_packed_async")
 
     def copy_packed_device(self, dev_ptr: int, to_lattice: bool, stream=None):
         if to_lattice:

@@ -205,40 +205,97 @@ def test_config2_4096x4096_one_sweep():
 @pytest.mark.parametrize("T,init", [(4, "block"), (8, "random")])
 def test_bench_lattice_65536_window_and_invariants(T, init):
     """BASELINE configs[4] lattice (65536 x 65536, what bench.py times; T = 8
-    with the random start is bench.py's own launch configuration: tile
-    kernel, cost-model tiles, 384-thread CTAs, TMA staging): invariants over
-    the whole lattice + sampled window parity for one pass."""
+    with the random start is bench.py's own launch configuration: the planar
+    tile kernel with its cost-model tiles, TMA staging): invariants over the
+    whole lattice + window parity for one full sweep (16 / T passes), with
+    windows at tile seams (rows k * THI) and inside each TMA box of an
+    interior band (the x seams lie inside every full-width window)."""
     from paper_1309_4349_b200 import kk
     Lx = Ly = 65536
     L = _lat(Lx, Ly, 0.5, 0.6, 99, init=kk.KK_INIT_BLOCK if init == "block" else kk.KK_INIT_RANDOM,
              iters_per_pass=T)
     pl = kk.plan(Lx, Ly, iters_per_pass=T)
-    assert pl["kernel"] == "tile" and (T != 8 or pl["threads"] == 640)   # tall tiles
+    assert pl["kernel"] == "planar" and pl["tma_boxes"] >= 1
     nA = L.composition()[0]
     assert nA == Lx * Ly // 2
     L.sweep(1)                                    # mix the block start
     nab0 = L.energy()[0][0]
     L.stats(reset=True)
-    hy = 3 * T
+    passes = 16 // T
+    hy = 3 * 16                                   # light cone of one sweep (R8)
     before = L.get_packed()[0]
     s = L.sweep_index()
-    L.run_pass(kk.REGION_ALL, None, None)         # iterations 0..3 of sweep s
-    L.pass_commit()
+    for _ in range(passes):                       # one sweep as single passes
+        L.run_pass(kk.REGION_ALL, None, None)
+        L.pass_commit()
     after = L.get_packed()[0]
     st = L.stats()[0]
     nab1 = L.energy()[0][0]
     assert L.composition()[0] == nA
     assert nab1 - nab0 == st[3]
-    assert st[0] == T * (Lx * Ly // 16)          # T iterations x N/16 centres
-    rng = np.random.default_rng(5)
-    for y0 in [0, Ly - 8, int(rng.integers(16, Ly - 16))]:
-        H = 8
+    assert st[0] == Lx * Ly                       # one sweep = N attempts (R11)
+    THI, HYp = pl["tile_rows"], pl["halo_rows"]
+    b = 5                                          # an interior band: staged rows b*THI - HYp ...
+    box_rows = [b * THI - HYp + 8, b * THI - HYp + 250, b * THI - HYp + min(300, THI + 2 * HYp - 16)]
+    seams = [0, THI - 4, 7 * THI - 4, Ly - 8]
+    H = 8
+    for y0 in seams + box_rows:
         rows = [(y0 - hy + r) % Ly for r in range(H + 2 * hy)]
         win = np.ascontiguousarray(inputs.unpack_rows(before[rows], Lx))
-        O.window_iterations(win, Ly, y0 - hy, 0.6, 99, s, 0, 0, T, hy, hy + H)
+        O.window_iterations(win, Ly, y0 - hy, 0.6, 99, s, 0, 0, 16, hy, hy + H)
         exp = win[hy:hy + H]
         got = inputs.unpack_rows(after[[(y0 + r) % Ly for r in range(H)]], Lx)
-        assert np.array_equal(got, exp)
+        assert np.array_equal(got, exp), y0
+
+
+def _forced_plan_parity(env, Lx, Ly, sweeps, kernel, boxes, monkeypatch, seed=777):
+    """Full-lattice multi-sweep parity of a launch plan forced through the
+    environment on a lattice the oracle finishes in seconds: 3 x 3 tiles, so
+    the middle tile is staged by TMA (all its rows and groups inside the
+    lattice) and the others exercise the x / y wrap through LDG."""
+    from paper_1309_4349_b200 import kk
+    for key, v in {**env, "KK_RESIDENT": 0, "KK_CLUSTER": 0, "KK_BAND": 0, "KK_TMA": 1}.items():
+        monkeypatch.setenv(key, str(v))
+    p = kk.plan(Lx, Ly, n_sm=0)
+    assert p["kernel"] == kernel and p["tiles_x"] == 3 and p["bands"] == 3, p
+    assert p["tile_words"] == int(env["KK_TWI"]) and p["tile_rows"] == int(env["KK_THI"]), p
+    assert p["tma_boxes"] == boxes, p
+    if "KK_PASS_THREADS" in env:
+        assert p["threads"] == int(env["KK_PASS_THREADS"])
+    _run_parity(Lx, Ly, 0.5, 0.6, seed, sweeps)
+
+
+def test_bench_plan_planar_full_parity(monkeypatch):
+    """bench.py's 65536^2 plan (the planar kernel's cost-model tiles, CTA size,
+    TMA boxes incl. the overlapped last box), forced on a 3 x 3-tile lattice."""
+    from paper_1309_4349_b200 import kk
+    pl = kk.plan(65536, 65536, n_sm=148)
+    assert pl["kernel"] == "planar"
+    env = {"KK_TWI": pl["tile_words"], "KK_THI": pl["tile_rows"], "KK_PASS_THREADS": pl["threads"],
+           "KK_PDL": pl["pass_pdl"], "KK_PLANAR": 2}
+    _forced_plan_parity(env, 3 * 32 * pl["tile_words"], 3 * pl["tile_rows"], 2, "planar", pl["tma_boxes"],
+                        monkeypatch)
+
+
+def test_bench_plan_planar_16384_full_parity(monkeypatch):
+    from paper_1309_4349_b200 import kk
+    pl = kk.plan(16384, 16384, n_sm=148)
+    assert pl["kernel"] == "planar"
+    env = {"KK_TWI": pl["tile_words"], "KK_THI": pl["tile_rows"], "KK_PASS_THREADS": pl["threads"],
+           "KK_PDL": pl["pass_pdl"], "KK_PLANAR": 2}
+    _forced_plan_parity(env, 3 * 32 * pl["tile_words"], 3 * pl["tile_rows"], 2, "planar", pl["tma_boxes"],
+                        monkeypatch)
+
+
+@pytest.mark.parametrize("twi,thi,nt,pdl,boxes", [(64, 596, 640, 0, 3), (64, 300, 512, 0, 2)])
+def test_tile_kernel_tall_and_16384_plans_full_parity(twi, thi, nt, pdl, boxes, monkeypatch):
+    """The row-major tile kernel's round-1 bench plan (64-word x 596-row tall
+    tiles, 640 threads, 3 TMA boxes with an overlapped last box) and its
+    16384^2 plan (300 rows, 512 threads, 2 boxes, PDL off), forced on 3 x 3
+    tiles: the kernel every lattice with Lx % 128 != 0 (and every small one)
+    runs."""
+    env = {"KK_TWI": twi, "KK_THI": thi, "KK_PASS_THREADS": nt, "KK_PDL": pdl, "KK_PLANAR": 0}
+    _forced_plan_parity(env, 3 * 32 * twi, 3 * thi, 2, "tile", boxes, monkeypatch)
 
 
 def test_bench_lattice_65536_cluster_histogram():
@@ -324,10 +381,12 @@ def test_tile_kernel_programmatic_dependent_launch(pdl, Lx, Ly, env, monkeypatch
     _run_parity(Lx, Ly, 0.5, 0.7, Lx + 17 * pdl, 4, R=2)
 
 
-def test_tile_kernel_640_threads_default_5120():
-    """5120^2 is a one-wave grid of 180 x 32 tiles: the plan takes 640-thread
-    CTAs (one per SM, up to 96 registers); one full sweep against the oracle."""
+def test_tile_kernel_640_threads_default_5120(monkeypatch):
+    """5120^2 is a one-wave grid of 180 x 32 tiles: the row-major tile kernel
+    (KK_PLANAR=0) takes 640-thread CTAs (one per SM, up to 96 registers); one
+    full sweep against the oracle."""
     from paper_1309_4349_b200 import kk
+    monkeypatch.setenv("KK_PLANAR", "0")
     p = kk.plan(5120, 5120)
     assert p["kernel"] == "tile" and p["threads"] == 640
     _run_parity(5120, 5120, 0.5, 0.6, 5120, 1)
@@ -360,9 +419,17 @@ def test_cluster_histogram_total_over_replicas():
         assert L.cluster_histogram_total(target) == sorted(tot.items())
 
 
-def test_8192_band_kernel_default():
-    """8192^2 runs on the band kernel (halos through L2 every 4 iterations)
-    by default; one full sweep must equal the oracle."""
+def test_8192_planar_default():
+    """8192^2 runs on the planar tile kernel by default (it replaced the band
+    kernel there); one full sweep must equal the oracle."""
     from paper_1309_4349_b200 import kk
-    assert kk.plan(8192, 8192, n_sm=0)["kernel"] == "band"
+    assert kk.plan(8192, 8192, n_sm=0)["kernel"] == "planar"
     _run_parity(8192, 8192, 0.5, 0.6, 8192, 1)
+
+
+def test_12288_band_kernel_default_when_not_planar():
+    """A lattice whose rows are not whole 128-site groups (Lx = 12000) takes
+    the band kernel at this size; two sweeps against the oracle."""
+    from paper_1309_4349_b200 import kk
+    assert kk.plan(12000, 8192, n_sm=0)["kernel"] == "band"
+    _run_parity(12000, 8192, 0.5, 0.6, 12000, 1)

@@ -23,7 +23,7 @@ from tests.test_gpu_parity import _gpu  # noqa: F401  (fixture)
 pytestmark = pytest.mark.gpu
 
 
-TILE_PATH = {"KK_RESIDENT": 0, "KK_CLUSTER": 0, "KK_BAND": 0}
+TILE_PATH = {"KK_RESIDENT": 0, "KK_CLUSTER": 0, "KK_BAND": 0, "KK_PLANAR": 2}
 
 
 @contextlib.contextmanager

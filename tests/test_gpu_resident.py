@@ -8,6 +8,8 @@ KK_RESIDENT=2 forces the resident kernel whenever the replica fits, 0 forces
 the tile kernel; the default (1) picks the resident kernel when the tile
 kernel would use <= 2 CTAs per replica.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -97,18 +99,26 @@ def test_resident_cta_sizes(Lx, Ly, R, nt):
     _run_parity(Lx, Ly, 0.4, 0.8, 5 + nt, 4, R=R, env={"KK_RESIDENT": 2, "KK_RES_THREADS": nt})
 
 
-# ---- band kernel (lattice spread over all SMs' shared memory, 3-row halo
-# exchange between neighbouring bands through L2 every iteration)
-@pytest.mark.parametrize("Lx,Ly", [(64, 64), (100, 40), (68, 16), (400, 400), (1000, 44), (2048, 64),
-                                   (4096, 600)])
+# ---- band kernel (lattice spread over all SMs' shared memory, 3*TB-row halos
+# exchanged between neighbouring bands through L2 every TB iterations)
+@pytest.mark.parametrize("Lx,Ly", [(1000, 1776), (2048, 1184), (400, 2368), (4096, 1776)])
 def test_band_kernel_matches_oracle(Lx, Ly):
-    _run_parity(Lx, Ly, 0.5, 0.7, Lx + 3 * Ly, 4, env={"KK_RESIDENT": 0, "KK_BAND": 2})
+    from paper_1309_4349_b200 import kk
+    env = {"KK_RESIDENT": 0, "KK_CLUSTER": 0, "KK_BAND": 2}
+    for key, v in env.items():
+        os.environ[key] = str(v)
+    try:
+        assert kk.plan(Lx, Ly, n_sm=0)["kernel"] == "band"
+    finally:
+        for key in env:
+            os.environ.pop(key, None)
+    _run_parity(Lx, Ly, 0.5, 0.7, Lx + 3 * Ly, 4, env=env)
 
 
 def test_band_kernel_mid_sweep_start_and_omega():
     from paper_1309_4349_b200 import kk
-    Lx, Ly, seed, om = 2048, 96, 99, 1.1
-    L = _lat(Lx, Ly, 0.4, om, seed, iters_per_pass=4, env={"KK_RESIDENT": 0, "KK_BAND": 2})
+    Lx, Ly, seed, om = 2048, 1184, 99, 1.1
+    L = _lat(Lx, Ly, 0.4, om, seed, iters_per_pass=4, env={"KK_RESIDENT": 0, "KK_CLUSTER": 0, "KK_BAND": 2})
     ref = O.init_random(Lx, Ly, 0.4, seed)
     L.run_pass(kk.REGION_ALL, None, None)      # tile kernel: iterations 0..3 of sweep 0
     L.pass_commit()
@@ -123,8 +133,8 @@ def test_band_kernel_mid_sweep_start_and_omega():
 
 def test_config2_4096_band_and_tile_agree():
     """BASELINE configs[2] (4096^2): the band kernel (KK_BAND=2, opt-in) and
-    the default tile kernel give the identical lattice and counters, equal to
-    the oracle's."""
+    the default (planar tile) kernel give the identical lattice and counters,
+    equal to the oracle's."""
     from paper_1309_4349_b200 import kk
     A = _lat(4096, 4096, 0.5, 0.6, 4096, init=kk.KK_INIT_RANDOM, env={"KK_BAND": 2})
     B = _lat(4096, 4096, 0.5, 0.6, 4096, init=kk.KK_INIT_RANDOM)

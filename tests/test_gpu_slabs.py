@@ -28,25 +28,22 @@ def _gpu():
 def _slabs(Lx, Ly, S, omega, seed, T, init_full=None, random_init=False, f=0.5):
     import torch
     from paper_1309_4349_b200 import kk
-    from paper_1309_4349_b200.distributed import select_choose
     rows = Ly // S
     labs = [kk.Lattice(Lx, Ly, f, omega, seed, init=kk.KK_INIT_EMPTY, iters_per_pass=T,
                        y_begin=s * rows, y_count=rows) for s in range(S)]
     if random_init:
-        # distributed exact-composition start: sum histograms over slabs
+        # distributed exact-composition start: sum histograms over slabs; the
+        # bin choice and the tie cut are the library's host steps
         nA = int(np.floor(f * Lx * Ly + 0.5))
         need = np.array([nA], np.int64)
-        prefix = np.zeros(1, np.int64)
+        prefix = np.zeros(1, np.uint32)
         for level in range(3):
-            h = sum(L.select_hist(level, None if level == 0 else (prefix & 0xFFFFFFFF).astype(np.uint32))
-                    for L in labs)
-            select_choose(level, h, need, prefix)
-        K = (prefix & 0xFFFFFFFF).astype(np.uint32)
-        ties = np.concatenate([L.select_ties(K) for L in labs])
-        idx = np.sort(ties[:, 1])
-        cut = np.array([idx[need[0] - 1] + 1 if need[0] > 0 else 0], np.int64)
+            h = sum(L.select_hist(level, None if level == 0 else prefix) for L in labs)
+            kk.select_choose(level, h, need, prefix)
+        ties = np.concatenate([L.select_ties(prefix) for L in labs])
+        cut = kk.select_cut(ties, 1, need)
         for L in labs:
-            L.select_apply(K, cut)
+            L.select_apply(prefix, cut)
     else:
         for s, L in enumerate(labs):
             L.set_lattice(init_full[s * rows:(s + 1) * rows][None])
@@ -77,17 +74,28 @@ def _run(labs, bufs, n_passes):
             L.pass_commit()
 
 
-@pytest.mark.parametrize("Lx,Ly,S,T,n", [(64, 96, 2, 4, 3), (72, 120, 3, 8, 2), (128, 64, 4, 2, 2),
-                                         (1024, 2048, 4, 8, 1), (2048, 512, 2, 8, 2)])
-def test_slab_passes_match_whole_lattice(Lx, Ly, S, T, n):
+@pytest.mark.parametrize("Lx,Ly,S,T,n,planar", [(64, 96, 2, 4, 3, 0), (72, 120, 3, 8, 2, 0), (128, 64, 4, 2, 2, 0),
+                                                (1024, 2048, 4, 8, 1, 0), (2048, 512, 2, 8, 2, 0),
+                                                (128, 64, 4, 2, 2, 2), (1024, 2048, 4, 8, 1, 2),
+                                                (2048, 512, 2, 8, 2, 2), (512, 384, 3, 4, 2, 2)])
+def test_slab_passes_match_whole_lattice(Lx, Ly, S, T, n, planar):
+    """Slab passes (halo pack, interior / boundary regions, halos received in
+    the public row-major layout) equal the whole-lattice oracle; planar=2
+    runs the planar tile kernel on the slabs (halo rows converted on staging,
+    kk_pack_halo converting planar rows back)."""
     import os
     os.environ["KK_THI"] = "8"          # several bands per slab: interior + boundary regions both used
+    os.environ["KK_PLANAR"] = str(planar)
     try:
         omega, seed = 0.7, 99
         full = O.init_random(Lx, Ly, 0.5, seed)
         labs, bufs = _slabs(Lx, Ly, S, omega, seed, T, init_full=full)
+        from paper_1309_4349_b200 import kk
+        assert kk.plan(Lx, Ly, y_begin=0, y_count=Ly // S, iters_per_pass=T)["kernel"] == (
+            "planar" if planar else "tile")
     finally:
         os.environ.pop("KK_THI", None)
+        os.environ.pop("KK_PLANAR", None)
     _run(labs, bufs, n * 16 // T)
     got = np.concatenate([L.get_lattice()[0] for L in labs])
     st = sum(L.stats()[0] for L in labs)

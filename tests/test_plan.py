@@ -17,7 +17,7 @@ SMEM_2_PER_SM = 113 * 1024     # two 512-thread tile CTAs per SM (228 KB per SM)
 def _lib():
     from paper_1309_4349_b200 import build
     build.build()
-    saved = {k: os.environ.pop(k, None) for k in ("KK_RESIDENT", "KK_BAND", "KK_THI", "KK_TWI", "KK_T",
+    saved = {k: os.environ.pop(k, None) for k in ("KK_RESIDENT", "KK_BAND", "KK_THI", "KK_TWI", "KK_T", "KK_PLANAR",
                                                   "KK_RES_THREADS", "KK_PASS_THREADS", "KK_CLUSTER", "KK_CLUSTER_TB",
                                                   "KK_BAND_TB")}
     yield
@@ -28,31 +28,43 @@ def _lib():
 
 def test_bench_lattice_plan(monkeypatch):
     p = kk.plan(65536, 65536)
-    assert p["kernel"] == "tile" and p["iters_per_pass"] == 8 and p["halo_rows"] == 24
-    assert p["tile_words"] == 64 and 540 <= p["tile_rows"] <= 600   # tall tiles, one per SM at a time
-    assert SMEM_2_PER_SM < p["smem_bytes"] <= 227 * 1024
-    assert p["ctas"] == p["tiles_x"] * p["bands"] >= 148 * 20
+    assert p["kernel"] == "planar" and p["iters_per_pass"] == 8 and p["halo_rows"] == 24
+    assert p["tile_words"] == 128 and 300 <= p["tile_rows"] <= 400   # widest TMA tile, as tall as fits
+    assert p["smem_bytes"] <= 227 * 1024 and p["tma_boxes"] >= 1
+    assert p["ctas"] == p["tiles_x"] * p["bands"] >= 148 * 16
     assert p["threads"] == 640
     assert p["pass_pdl"] == 0                       # early CTAs would idle in slots
+    # the row-major tile kernel's plan (KK_PLANAR=0; every lattice with Lx % 128 != 0)
+    monkeypatch.setenv("KK_PLANAR", "0")
+    t = kk.plan(65536, 65536)
+    assert t["kernel"] == "tile" and t["tile_words"] == 64 and 540 <= t["tile_rows"] <= 600
+    assert SMEM_2_PER_SM < t["smem_bytes"] <= 227 * 1024 and t["threads"] == 640 and t["pass_pdl"] == 0
     monkeypatch.setenv("KK_TALL", "0")              # two CTAs per SM: the cost-model tiles
     q = kk.plan(65536, 65536)
     monkeypatch.delenv("KK_TALL")
     assert q["tile_words"] == 64 and 300 <= q["tile_rows"] <= 340 and q["smem_bytes"] <= SMEM_2_PER_SM
     assert q["threads"] == 384                      # many waves: 80-register CTAs
     assert kk.plan(16384, 16384)["threads"] == 512  # too few waves for tall tiles
+    monkeypatch.delenv("KK_PLANAR")
 
 
-def test_mid_size_lattice_fills_every_sm():
+def test_mid_size_lattice_fills_every_sm(monkeypatch):
     p = kk.plan(4096, 4096)
-    assert p["kernel"] == "tile" and p["ctas"] >= 148
+    assert p["kernel"] == "planar" and p["ctas"] >= 128
     assert p["pass_pdl"] == 1                       # one wave: next pass launches under this one
-    assert kk.plan(5120, 5120)["threads"] == 640    # one wave, > 384 items per iteration
-    assert p["threads"] == 640                      # 4096^2 likewise
-    r = kk.plan(2048, 2048)                         # one wave, every iteration one round of 384 items
+    assert kk.plan(5120, 5120)["kernel"] == "planar"
+    r = kk.plan(2048, 2048)                         # too few 32-centre items: row-major tile kernel
     assert r["kernel"] == "tile" and r["ctas"] <= 296 and r["threads"] == 384 and r["pass_pdl"] == 1
-    q = kk.plan(8192, 8192)                      # band kernel: one band per SM, L2 halos every 4 iterations
+    assert kk.plan(8192, 8192)["kernel"] == "planar"   # the planar kernel replaced the band kernel
+    assert kk.plan(16384, 16384)["kernel"] == "planar"
+    q = kk.plan(12000, 8192)                        # rows not whole 128-site groups: band kernel
     assert q["kernel"] == "band" and q["ctas"] == 148 and q["threads"] == 1024
+    monkeypatch.setenv("KK_PLANAR", "0")
+    assert kk.plan(8192, 8192)["kernel"] == "band"
+    assert kk.plan(4096, 4096)["threads"] == 640    # one wave, > 384 items per iteration
     assert kk.plan(16384, 16384)["kernel"] == "tile"   # bands no longer fit in shared memory
+    monkeypatch.setenv("KK_PLANAR", "2")            # planar whenever the rows allow
+    assert kk.plan(1024, 1024)["kernel"] == "planar"
 
 
 def test_small_and_replica_batches_are_resident():
@@ -75,7 +87,7 @@ def test_small_and_replica_batches_are_resident():
 
 def test_slabs_never_use_the_resident_or_band_kernels():
     p = kk.plan(65536, 8 * 65536, y_begin=65536, y_count=65536)
-    assert p["kernel"] == "tile"
+    assert p["kernel"] == "planar"
     q = kk.plan(400, 800, y_begin=400, y_count=400)
     assert q["kernel"] == "tile"
 
@@ -92,7 +104,7 @@ def test_overrides(monkeypatch):
     assert kk.plan(4096, 4096)["kernel"] == "band"
     assert kk.plan(4096, 4096)["ctas"] == 148
     monkeypatch.setenv("KK_BAND", "0")
-    assert kk.plan(8192, 8192)["kernel"] == "tile"
+    assert kk.plan(12000, 8192)["kernel"] == "tile"
     monkeypatch.delenv("KK_BAND")
     monkeypatch.delenv("KK_RESIDENT")
     monkeypatch.setenv("KK_THI", "64")
@@ -120,6 +132,10 @@ def test_plan_invariants(Lx, Ly, R, T):
     if p["kernel"] == "tile":
         assert p["ctas"] == p["tiles_x"] * p["bands"] * R
         assert p["smem_bytes"] <= SMEM_2_PER_SM or os.environ.get("KK_THI") or p["threads"] == 640
+    elif p["kernel"] == "planar":
+        assert Lx % 128 == 0 and Lx * Ly * R >= 1 << 24
+        assert p["ctas"] == p["tiles_x"] * p["bands"] * R and p["tile_words"] % 4 == 0
+        assert p["threads"] in (512, 640, 768, 896)
     elif p["kernel"] == "resident":
         assert p["ctas"] == R and Lx >= 64 and p["threads"] in (128, 256, 512)
     elif p["kernel"] == "cluster":

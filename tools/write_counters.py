@@ -1,5 +1,7 @@
 """Write profiles/pass_kernel_counters.json (read by bench.py for the roofline)
-from an ncu --set full capture of one bench-lattice pass.
+from an ncu --set full capture of one bench-lattice pass, stamped with the
+launch plan it was captured under (kk_plan_config of the 65536^2 bench lattice
+on a 148-SM B200): bench.py refuses the counters if its own plan differs.
 Usage: python tools/write_counters.py report.ncu-rep updates_per_launch "tile description" [out.json]"""
 import csv
 import io
@@ -7,6 +9,9 @@ import json
 import os
 import subprocess
 import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1309_4349_b200 import kk  # noqa: E402
 
 rep, upd, tile = sys.argv[1], float(sys.argv[2]), sys.argv[3]
 out = sys.argv[4] if len(sys.argv) > 4 else os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
@@ -34,6 +39,8 @@ d = {
     "fma_pipe_pct": round(val("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"), 2),
     "source": f"ncu --set full --clock-control none, tools/profile_pass.py 65536 65536 1 8 (bench lattice); {os.path.basename(rep)}",
     "tile": tile,
+    "plan": {k: v for k, v in kk.plan(65536, 65536, iters_per_pass=8, n_sm=148).items()
+             if k in ("kernel", "iters_per_pass", "tile_words", "tile_rows", "threads", "tma_boxes")},
 }
 with open(out, "w") as f:
     json.dump(d, f, indent=1)
