@@ -120,13 +120,19 @@ __device__ __forceinline__ void hist_add(const CclParams& P, int64_t rep, unsign
 // run pair and bond type ((0,+1) and (+1,+1)): a union point is placed where
 // the overlap starts, i.e. at a run start of either row.
 
-// First site (tile index) of the run containing target site x of row r.
-__device__ __forceinline__ uint32_t run_start(const uint32_t* S, int r, int x) {
-    int wi = x >> 5;
-    uint32_t m = S[r * kTW + wi] & (0xFFFFFFFFu >> (31 - (x & 31)));
-    while (m == 0) m = S[r * kTW + (--wi)];
-    return (uint32_t)(r * kTX + 32 * wi + 31 - __clz(m));
+// First site (tile index) of the run containing target site x of row r: the
+// last run start at or below x in x's word, else the carry of the word (the
+// start of the run that enters the word at bit 0, tabulated per word).
+__device__ __forceinline__ uint32_t run_start(const uint32_t* S, const uint32_t* C, int r, int x) {
+    const int wi = x >> 5;
+    const uint32_t m = S[r * kTW + wi] & (0xFFFFFFFFu >> (31 - (x & 31)));
+    return m ? (uint32_t)(r * kTX + 32 * wi + 31 - __clz(m)) : C[r * kTW + wi];
 }
+
+// Cluster sizes below kSmallHist are counted in a per-CTA shared histogram and
+// flushed with one global atomic per nonzero bin (most clusters are small:
+// per-cluster global atomics on a few hot bins serialised in L2).
+constexpr int kSmallHist = 256;
 
 __global__ void __launch_bounds__(kThreads) ccl_tile_kernel(const CclParams P) {
     extern __shared__ uint32_t smem[];
@@ -137,7 +143,9 @@ __global__ void __launch_bounds__(kThreads) ccl_tile_kernel(const CclParams P) {
     uint32_t* cnt32 = lab + kSites;      // [kSites/2] 16-bit size per root (two per word), then node index
     uint16_t* cnt = reinterpret_cast<uint16_t*>(cnt32);
     uint16_t* node_s = reinterpret_cast<uint16_t*>(cnt32 + kSites / 2);  // [kEdge]
+    uint32_t* C = cnt32 + kSites / 2 + kEdge / 2;                         // [kTR*kTW] run carry per word
     __shared__ unsigned int n_nodes, node_base;
+    __shared__ unsigned int shist[kSmallHist];
 
     const Geom& g = P.g;
     const int tx = blockIdx.x, ty = blockIdx.y;
@@ -149,6 +157,7 @@ __global__ void __launch_bounds__(kThreads) ccl_tile_kernel(const CclParams P) {
     const uint32_t tmask = P.target ? 0u : 0xFFFFFFFFu;
 
     if (threadIdx.x == 0) n_nodes = 0;
+    for (int i = threadIdx.x; i < kSmallHist; i += kThreads) shist[i] = 0u;
     for (int i = threadIdx.x; i < kTR * kTW; i += kThreads) {
         const int r = i / kTW, w = i - r * kTW;
         uint32_t v = 0;
@@ -170,6 +179,16 @@ __global__ void __launch_bounds__(kThreads) ccl_tile_kernel(const CclParams P) {
         for (uint32_t m = st; m; m &= m - 1) {
             const int b = __ffs(m) - 1;
             lab[base + b] = base + b;
+        }
+    }
+    __syncthreads();
+    // run carry per word: the last run start left of the word in its row
+    for (int r = threadIdx.x; r < kTR; r += kThreads) {
+        uint32_t last = kNone;
+        for (int w = 0; w < kTW; ++w) {
+            C[r * kTW + w] = last;
+            const uint32_t st = S[r * kTW + w];
+            if (st) last = (uint32_t)(r * kTX + 32 * w + 31 - __clz(st));
         }
     }
     __syncthreads();
@@ -216,7 +235,7 @@ __global__ void __launch_bounds__(kThreads) ccl_tile_kernel(const CclParams P) {
             for (uint32_t j = lane; j < cnt_r; j += 32) {
                 const uint32_t e = ubuf[j];
                 const int er = (int)(e >> 9), ex = (int)((e >> 1) & 255u);
-                union32(lab, run_start(S, er, ex), run_start(S, er + 1, ex + (int)(e & 1u)));
+                union32(lab, run_start(S, C, er, ex), run_start(S, C, er + 1, ex + (int)(e & 1u)));
             }
             __syncwarp();
         }
@@ -237,7 +256,7 @@ __global__ void __launch_bounds__(kThreads) ccl_tile_kernel(const CclParams P) {
             m &= ~seg;
             const int x0 = 32 * w + __ffs(seg) - 1;
             const int x1 = 32 * w + 31 - __clz(seg);
-            const uint32_t root = root_of(lab, run_start(S, r, x0));
+            const uint32_t root = root_of(lab, run_start(S, C, r, x0));
             atomicAdd(&cnt32[root >> 1], (uint32_t)__popc(seg) << (16 * (root & 1)));
             if (edge_row || x0 == 0 || x1 == w_tile - 1) atomicOr(&touch[root >> 5], 1u << (root & 31));
         }
@@ -254,12 +273,16 @@ __global__ void __launch_bounds__(kThreads) ccl_tile_kernel(const CclParams P) {
                 const unsigned int k = atomicAdd(&n_nodes, 1u);
                 node_s[k] = (uint16_t)sz;
                 cnt[s0] = k;   // root -> local node index
+            } else if (sz < kSmallHist) {
+                atomicAdd(&shist[sz], 1u);
             } else {
                 hist_add(P, rep, sz);
             }
         }
     }
     __syncthreads();
+    for (int i = threadIdx.x; i < kSmallHist; i += kThreads)
+        if (shist[i]) atomicAdd(P.hist + rep * kDense + i, shist[i]);
     if (threadIdx.x == 0) node_base = atomicAdd(P.node_count, n_nodes);
     __syncthreads();
     const unsigned int base = node_base;
@@ -282,7 +305,7 @@ __global__ void __launch_bounds__(kThreads) ccl_tile_kernel(const CclParams P) {
         else { r = e - 2 * kTX - kTR; x = w_tile - 1; }                  // right column
         uint32_t v = kNone;
         if (r < h_tile && x < w_tile && ((tb[r * kTW + (x >> 5)] >> (x & 31)) & 1u))
-            v = base + cnt[root_of(lab, run_start(S, r, x))];
+            v = base + cnt[root_of(lab, run_start(S, C, r, x))];
         E[e] = v;
     }
 }
@@ -477,7 +500,7 @@ cudaError_t launch_ccl(const uint32_t* lat, const Geom& g, int64_t replicas, int
     P.node_cap = ccl_node_cap(g, replicas);
     cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(unsigned int), s);
     if (e != cudaSuccess) return e;
-    const int smem = 4 * (2 * kTR * kTW + kSites / 32 + kSites + kSites / 2) + 2 * kEdge;
+    const int smem = 4 * (2 * kTR * kTW + kSites / 32 + kSites + kSites / 2 + kEdge / 2 + kTR * kTW);
     e = ensure_dynamic_smem((const void*)ccl_tile_kernel, smem);
     if (e != cudaSuccess) return e;
     ccl_tile_kernel<<<dim3(P.tiles_x, P.tiles_y, (unsigned)replicas), kThreads, smem, s>>>(P);

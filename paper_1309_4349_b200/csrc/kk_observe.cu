@@ -21,52 +21,83 @@ __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
 }
 
 // ---- energy (N_AB) and composition ------------------------------------------
-// grid = (bx, replicas in this launch); each CTA reduces its share of one
-// replica: warp shuffle -> shared memory -> one 64-bit atomic per counter.
-__global__ void observe_kernel(const ObsParams P, int64_t rep0) {
-    __shared__ unsigned long long red[2][8];
+// One warp per row (grid-stride over rows of all replicas in the launch): the
+// lanes stream the row and the row above in 16-byte vectors, the x+1 view of
+// the last word of a vector comes from the next lane by shuffle (lane 31
+// loads it), so every site is read once and no division or per-site branch is
+// issued.  Rows with a partial last word (Lx % 32 != 0) take the generic path
+// (get32 with the periodic wrap).  Three forward bonds per site as XOR +
+// popcount, warp-shuffle reduction, one 64-bit atomic per warp.
+__device__ __forceinline__ void obs_row_fast(const uint32_t* row, const uint32_t* up, int64_t W, int lane,
+                                             unsigned long long& nab, unsigned long long& na) {
+    // W % 4 == 0, tail == 0: vectors of 4 words; x+1 of word k = (w_k >> 1) | (w_{k+1} << 31)
+    const uint4* r4 = reinterpret_cast<const uint4*>(row);
+    const uint4* u4 = up ? reinterpret_cast<const uint4*>(up) : nullptr;
+    const int64_t nv = W / 4;
+    for (int64_t v0 = 0; v0 < nv; v0 += 32) {
+        const int64_t v = v0 + lane;
+        const bool ok = v < nv;
+        const uint4 a = ok ? r4[v] : make_uint4(0, 0, 0, 0);
+        const uint4 b = (ok && u4) ? u4[v] : make_uint4(0, 0, 0, 0);
+        // first word of the next vector (periodic at the row end)
+        uint32_t an = __shfl_down_sync(0xFFFFFFFFu, a.x, 1), bn = __shfl_down_sync(0xFFFFFFFFu, b.x, 1);
+        if (ok && (lane == 31 || v + 1 >= nv)) {
+            const int64_t vn = v + 1 >= nv ? 0 : v + 1;
+            an = row[4 * vn];
+            bn = u4 ? up[4 * vn] : 0u;
+        }
+        if (!ok) continue;
+        const uint32_t a1x = __funnelshift_r(a.x, a.y, 1), a1y = __funnelshift_r(a.y, a.z, 1);
+        const uint32_t a1z = __funnelshift_r(a.z, a.w, 1), a1w = __funnelshift_r(a.w, an, 1);
+        na += __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w);
+        nab += __popc(a.x ^ a1x) + __popc(a.y ^ a1y) + __popc(a.z ^ a1z) + __popc(a.w ^ a1w);  // (+1, 0)
+        if (u4) {
+            const uint32_t b1x = __funnelshift_r(b.x, b.y, 1), b1y = __funnelshift_r(b.y, b.z, 1);
+            const uint32_t b1z = __funnelshift_r(b.z, b.w, 1), b1w = __funnelshift_r(b.w, bn, 1);
+            nab += __popc(a.x ^ b.x) + __popc(a.y ^ b.y) + __popc(a.z ^ b.z) + __popc(a.w ^ b.w);    // (0, +1)
+            nab += __popc(a.x ^ b1x) + __popc(a.y ^ b1y) + __popc(a.z ^ b1z) + __popc(a.w ^ b1w);  // (+1, +1)
+        }
+    }
+}
+
+__global__ void observe_kernel(const ObsParams P, int64_t rep0, int64_t nrep) {
     const Geom& g = P.g;
-    const int64_t rep = rep0 + blockIdx.y;
-    const int64_t per_rep = g.rows * g.W;
-    const uint32_t* lat = P.lat + rep * g.rep_words;
-    unsigned long long nab = 0, na = 0;
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < per_rep;
-         k += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t y = k / g.W;
-        const int64_t gw = k - y * g.W;
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int64_t total_rows = g.rows * nrep;
+    const bool fast = g.tail == 0 && g.W % 4 == 0;
+    for (int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); k < total_rows; k += warps) {
+        const int64_t rl = k / g.rows;  // one division per row
+        const int64_t y = k - rl * g.rows, rep = rep0 + rl;
+        const uint32_t* lat = P.lat + rep * g.rep_words;
         const uint32_t* row = lat + y * g.W;
         const uint32_t* up;
-        if (y + 1 < g.rows) {
-            up = row + g.W;
-        } else if (g.periodic) {
-            up = lat;  // wraps to row 0
+        if (y + 1 < g.rows) up = row + g.W;
+        else if (g.periodic) up = lat;  // wraps to row 0
+        else up = P.halo_bot ? P.halo_bot + rep * P.halo_stride : nullptr;
+        unsigned long long nab = 0, na = 0;
+        if (fast) {
+            obs_row_fast(row, up, g.W, lane, nab, na);
         } else {
-            up = P.halo_bot ? P.halo_bot + rep * P.halo_stride : nullptr;
+            for (int64_t gw = lane; gw < g.W; gw += 32) {
+                const uint32_t mask = word_mask(g, gw);
+                const uint32_t a = row[gw];
+                const uint32_t a1 = get32(row, 32 * gw + 1, g);  // sites x+1
+                na += __popc(a & mask);
+                nab += __popc((a ^ a1) & mask);
+                if (up) {
+                    const uint32_t b = up[gw];
+                    const uint32_t b1 = get32(up, 32 * gw + 1, g);
+                    nab += __popc((a ^ b) & mask) + __popc((a ^ b1) & mask);
+                }
+            }
         }
-        const uint32_t mask = word_mask(g, gw);
-        const uint32_t a = row[gw];
-        const uint32_t a1 = get32(row, 32 * gw + 1, g);  // sites x+1
-        na += __popc(a & mask);
-        nab += __popc((a ^ a1) & mask);                   // bond (+1, 0)
-        if (up) {
-            const uint32_t b = up[gw];
-            const uint32_t b1 = get32(up, 32 * gw + 1, g);
-            nab += __popc((a ^ b) & mask);                // bond (0, +1)
-            nab += __popc((a ^ b1) & mask);               // bond (+1, +1)
+        nab = warp_sum(nab);
+        na = warp_sum(na);
+        if (lane == 0) {
+            if (nab) atomicAdd(P.out + 2 * rep, nab);
+            if (na) atomicAdd(P.out + 2 * rep + 1, na);
         }
-    }
-    nab = warp_sum(nab);
-    na = warp_sum(na);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (lane == 0) {
-        red[0][warp] = nab;
-        red[1][warp] = na;
-    }
-    __syncthreads();
-    if (threadIdx.x < 2) {
-        unsigned long long s = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[threadIdx.x][w];
-        if (s) atomicAdd(P.out + 2 * rep + threadIdx.x, s);
     }
 }
 
@@ -214,15 +245,12 @@ int grid_for(int64_t n, int threads) {
 }  // namespace
 
 cudaError_t launch_observe(const ObsParams& P, cudaStream_t s) {
-    const int64_t per = P.g.rows * P.g.W;
-    for (int64_t r0 = 0; r0 < P.replicas; r0 += 65535) {
-        const int64_t nrep = (P.replicas - r0) < 65535 ? (P.replicas - r0) : 65535;
-        int bx = grid_for(per, 256);
-        const int64_t cap = (148 * 16 + nrep - 1) / nrep;
-        if (bx > cap) bx = (int)cap;
-        observe_kernel<<<dim3(bx, (unsigned)nrep), 256, 0, s>>>(P, r0);
-        count_launch();
-    }
+    // 8 warps per CTA, up to 16 CTAs per SM worth of rows
+    const int64_t rows = P.g.rows * P.replicas;
+    int64_t ctas = (rows + 7) / 8;
+    if (ctas > 148 * 16) ctas = 148 * 16;
+    observe_kernel<<<(unsigned)(ctas < 1 ? 1 : ctas), 256, 0, s>>>(P, 0, P.replicas);
+    count_launch();
     return cudaGetLastError();
 }
 

@@ -37,7 +37,8 @@ d = {
     "issue_active_pct": round(val("smsp__issue_active.avg.pct_of_peak_sustained_active"), 2),
     "alu_pipe_pct": round(val("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"), 2),
     "fma_pipe_pct": round(val("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"), 2),
-    "source": f"ncu --set full --clock-control none, tools/profile_pass.py 65536 65536 1 8 (bench lattice); {os.path.basename(rep)}",
+    "source": os.environ.get("KK_COUNTERS_SOURCE", f"ncu --set full --clock-control none of the bench lattice; "
+                                                    f"{os.path.basename(rep)}"),
     "tile": tile,
     "plan": {k: v for k, v in kk.plan(65536, 65536, iters_per_pass=8, n_sm=148).items()
              if k in ("kernel", "iters_per_pass", "tile_words", "tile_rows", "threads", "tma_boxes")},
