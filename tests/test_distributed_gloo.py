@@ -225,7 +225,9 @@ def _worker(rank, world, port, cfg, q):
 
 
 @pytest.mark.parametrize("world,Lx,Ly,T,n", [(2, 16, 48, 4, 3), (2, 8, 32, 2, 2), (4, 16, 96, 4, 2),
-                                              (2, 24, 40, 1, 2)])
+                                              (2, 24, 40, 1, 2),
+                                              # strong scaling: one 16 x 96 lattice over 2, 4 and 8 ranks
+                                              (2, 16, 96, 4, 1), (8, 16, 96, 4, 1)])
 def test_slab_driver_matches_single_lattice(world, Lx, Ly, T, n):
     omega, seed, f = 0.7, 4321, 0.45
     ctx = mp.get_context("spawn")
@@ -255,3 +257,13 @@ def test_slab_driver_matches_single_lattice(world, Lx, Ly, T, n):
     assert obs["clusters_A"] == sum(c for _, c in O.cluster_histogram(ref, 1))
     for r in res[1:]:
         assert r[3]["hist"][1] is None                   # only rank 0 assembles the histogram
+
+
+def test_slab_rows_rejects_uneven_splits():
+    """make_simulation's split: equal slabs whose height is a multiple of 4
+    (R10); anything else would leave rows unsimulated."""
+    from paper_1309_4349_b200.distributed import slab_rows
+    assert slab_rows(65536, 8) == 8192 and slab_rows(96, 8) == 12
+    for Ly, world in [(1028, 8), (100, 3), (96, 16), (96, 0)]:
+        with pytest.raises(ValueError):
+            slab_rows(Ly, world)
