@@ -343,8 +343,10 @@ void choose_tiles_planar(kk_lattice* h, int nsm) {
             const int NG = h->TWI / 4 + 2;
             double work = 0.0;
             for (int t = 0; t < T; ++t) {
+                // the SM is issue-bound: time ~ items, plus part of a ragged last round
                 const double rows = (h->THI + 3.0 * (T - 1 - t) + 2.0) / 4.0;
-                work += std::ceil(std::ceil(rows) * NG / NT);
+                const double rounds = std::ceil(rows) * NG / NT;
+                work += rounds + 0.3 * (std::ceil(rounds) - rounds);
             }
             work += 0.05 * (double)(h->THI + 6 * T) * NG / NT + 1.0;  // staging (TMA) + fixed
             const int64_t ctas = (int64_t)h->tiles_x * h->bands * h->R;
