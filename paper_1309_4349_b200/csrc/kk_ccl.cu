@@ -26,12 +26,16 @@ namespace kk {
 
 namespace {
 
-constexpr int kTR = 64;                    // tile rows
+#ifndef KK_CCL_ROWS
+#define KK_CCL_ROWS 64
+#endif
+constexpr int kTR = KK_CCL_ROWS;           // tile rows
 constexpr int kTW = 8;                     // tile words per row (256 sites)
 constexpr int kTX = 32 * kTW;              // tile sites per row
 constexpr int kSites = kTR * kTX;          // 16384 (16-bit local sizes)
 constexpr int kEdge = 2 * kTX + 2 * kTR;   // edge entries per tile
-constexpr int kThreads = 512;  // one thread per tile word in the per-word phases
+constexpr int kThreads = kTR * kTW;  // one thread per tile word in the per-word phases
+static_assert(kSites <= 65535 && kThreads <= 1024, "16-bit local sizes, one thread per tile word");
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 // 32-bit labels in shared memory: sub-word CAS is emulated by a CAS loop on the
 // containing word, which races with the plain 16-bit stores of path halving.

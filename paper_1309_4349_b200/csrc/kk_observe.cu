@@ -34,6 +34,7 @@ __device__ __forceinline__ void obs_row_fast(const uint32_t* row, const uint32_t
     const uint4* r4 = reinterpret_cast<const uint4*>(row);
     const uint4* u4 = up ? reinterpret_cast<const uint4*>(up) : nullptr;
     const int64_t nv = W / 4;
+#pragma unroll 4
     for (int64_t v0 = 0; v0 < nv; v0 += 32) {
         const int64_t v = v0 + lane;
         const bool ok = v < nv;
