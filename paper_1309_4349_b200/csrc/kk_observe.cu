@@ -22,10 +22,9 @@ __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
 
 // ---- energy (N_AB) and composition ------------------------------------------
 // One warp per row (grid-stride over rows of all replicas in the launch): the
-// lanes stream the row and the row above in 16-byte vectors, the x+1 view of
-// the last word of a vector comes from the next lane by shuffle (lane 31
-// loads it), so every site is read once and no division or per-site branch is
-// issued.  Rows with a partial last word (Lx % 32 != 0) take the generic path
+// lanes stream the row and the row above in 16-byte vectors (plus the first
+// word of the next vector, an L1 hit), so every site is read once from HBM and
+// no division or per-site branch is issued.  Rows with a partial last word (Lx % 32 != 0) take the generic path
 // (get32 with the periodic wrap).  Three forward bonds per site as XOR +
 // popcount, warp-shuffle reduction, one 64-bit atomic per warp.
 __device__ __forceinline__ void obs_row_fast(const uint32_t* row, const uint32_t* up, int64_t W, int lane,
@@ -40,13 +39,11 @@ __device__ __forceinline__ void obs_row_fast(const uint32_t* row, const uint32_t
         const bool ok = v < nv;
         const uint4 a = ok ? r4[v] : make_uint4(0, 0, 0, 0);
         const uint4 b = (ok && u4) ? u4[v] : make_uint4(0, 0, 0, 0);
-        // first word of the next vector (periodic at the row end)
-        uint32_t an = __shfl_down_sync(0xFFFFFFFFu, a.x, 1), bn = __shfl_down_sync(0xFFFFFFFFu, b.x, 1);
-        if (ok && (lane == 31 || v + 1 >= nv)) {
-            const int64_t vn = v + 1 >= nv ? 0 : v + 1;
-            an = row[4 * vn];
-            bn = u4 ? up[4 * vn] : 0u;
-        }
+        // first word of the next vector (periodic at the row end; an L1 hit:
+        // the next lane loads the same line)
+        const int64_t vn = v + 1 >= nv ? 0 : v + 1;
+        const uint32_t an = ok ? row[4 * vn] : 0u;
+        const uint32_t bn = (ok && u4) ? up[4 * vn] : 0u;
         if (!ok) continue;
         const uint32_t a1x = __funnelshift_r(a.x, a.y, 1), a1y = __funnelshift_r(a.y, a.z, 1);
         const uint32_t a1z = __funnelshift_r(a.z, a.w, 1), a1w = __funnelshift_r(a.w, an, 1);
