@@ -79,12 +79,13 @@ int64_t ccl_edge_entries(const Geom& g, int64_t replicas);
 int64_t ccl_node_cap(const Geom& g, int64_t replicas);
 cudaError_t launch_ccl(const uint32_t* lat, const Geom& g, int64_t replicas, int target, uint32_t* edges,
                        uint32_t* node_size, uint32_t* node_par, uint32_t* node_rep,
-                       unsigned long long* root_size, unsigned int* counter, unsigned int* hist,
+                       unsigned long long* root_size, unsigned int* counter, unsigned int* hist, int64_t dense,
                        unsigned long long* big, unsigned long long* nbig, int64_t big_cap, cudaStream_t s,
                        const SlabCclArgs* slab);
-cudaError_t launch_hist_compact(const unsigned int* hist, int64_t R, unsigned int* rep_rows,
+int64_t hist_chunks(int64_t R, int64_t dense);
+cudaError_t launch_hist_compact(const unsigned int* hist, int64_t R, int64_t dense, unsigned int* chunk_rows,
                                 unsigned long long* row_off, cudaStream_t s);
-cudaError_t launch_hist_emit(const unsigned int* hist, int64_t R, const unsigned long long* row_off,
+cudaError_t launch_hist_emit(const unsigned int* hist, int64_t R, int64_t dense, const unsigned long long* row_off,
                              unsigned long long* rows, cudaStream_t s);
 cudaError_t launch_join(int64_t Lx, int64_t nslabs, const uint32_t* top, const uint32_t* bot, const uint32_t* off,
                         const unsigned long long* sizes, int64_t n, uint32_t* par, unsigned long long* rsize,
@@ -139,8 +140,9 @@ struct kk_lattice {
     unsigned long long* big = nullptr;
     unsigned long long* nbig = nullptr;
     int64_t big_cap = 0;
-    unsigned int* rep_rows = nullptr;       // [R] nonzero dense bins per replica
-    unsigned long long* row_off = nullptr;  // [R+1] their exclusive scan
+    int64_t dense = 0;                      // dense histogram bins per replica (multiple of 1024)
+    unsigned int* rep_rows = nullptr;       // [R * dense/1024] nonzero dense bins per chunk
+    unsigned long long* row_off = nullptr;  // [R * dense/1024 + 1] their exclusive scan
     unsigned long long* rows_buf = nullptr; // compact dense rows (size << 32 | count)
     int64_t rows_cap = 0;
     // double-buffered host I/O (lazy)
@@ -1177,15 +1179,22 @@ int ensure_ccl_workspace(kk_lattice* h) {
     if (h->edges) return KK_OK;
     const int64_t n = h->g.Lx * h->g.rows * h->R;
     const int64_t ne = ccl_edge_entries(h->g, h->R), nn = ccl_node_cap(h->g, h->R);
-    h->big_cap = n / kDense + 16;
+    // dense bins: every size below the bin count is histogrammed on the device
+    // (only larger clusters go to the (replica, size) list sorted on the host);
+    // 4096 bins per replica, up to 2^20 for a single big lattice (4 MB)
+    h->dense = kDense;
+    while (h->dense < ((int64_t)1 << 20) && h->dense * 64 < n / h->R && h->dense * 2 * h->R * 4 <= ((int64_t)16 << 20))
+        h->dense *= 2;
+    const int64_t nch = hist_chunks(h->R, h->dense);
+    h->big_cap = n / h->dense + 16;
     if (cudaMalloc(&h->edges, 4 * ne) || cudaMalloc(&h->node_size, 4 * nn) || cudaMalloc(&h->node_par, 4 * nn) ||
         cudaMalloc(&h->node_rep, 4 * nn) || cudaMalloc(&h->root_size, 8 * nn) ||
         cudaMalloc(&h->counter, sizeof(unsigned int)) || cudaMalloc(&h->open_flag, 4 * nn) ||
         cudaMalloc(&h->compact, 4 * nn) || cudaMalloc(&h->open_count, sizeof(unsigned int)) ||
-        cudaMalloc(&h->hist, sizeof(unsigned int) * kDense * h->R) ||
+        cudaMalloc(&h->hist, sizeof(unsigned int) * h->dense * h->R) ||
         cudaMalloc(&h->big, sizeof(unsigned long long) * 2 * h->big_cap) ||
-        cudaMalloc(&h->nbig, sizeof(unsigned long long)) || cudaMalloc(&h->rep_rows, sizeof(unsigned int) * h->R) ||
-        cudaMalloc(&h->row_off, sizeof(unsigned long long) * (h->R + 1))) {
+        cudaMalloc(&h->nbig, sizeof(unsigned long long)) || cudaMalloc(&h->rep_rows, sizeof(unsigned int) * nch) ||
+        cudaMalloc(&h->row_off, sizeof(unsigned long long) * (nch + 1))) {
         cudaGetLastError();
         // release the partial workspace so that a later call starts over
         void** ws[] = {(void**)&h->edges, (void**)&h->node_size, (void**)&h->node_par, (void**)&h->node_rep,
@@ -1204,14 +1213,14 @@ int ensure_ccl_workspace(kk_lattice* h) {
 // Dense histogram + big list -> rows (replica, size, count) sorted.  The
 // dense part is compacted on the device (only nonzero bins are copied back).
 int collect_hist_rows(kk_lattice* h, cudaStream_t s, std::vector<int64_t>& rows) {
-    const int64_t R = h->R;
-    KK_CUDA(launch_hist_compact(h->hist, R, h->rep_rows, h->row_off, s));
+    const int64_t R = h->R, nch = hist_chunks(R, h->dense), cpr = nch / R;  // chunks per replica
+    KK_CUDA(launch_hist_compact(h->hist, R, h->dense, h->rep_rows, h->row_off, s));
     unsigned long long total = 0, nb = 0;
-    KK_CUDA(cudaMemcpyAsync(&total, h->row_off + R, sizeof(total), cudaMemcpyDeviceToHost, s));
+    KK_CUDA(cudaMemcpyAsync(&total, h->row_off + nch, sizeof(total), cudaMemcpyDeviceToHost, s));
     KK_CUDA(cudaMemcpyAsync(&nb, h->nbig, sizeof(nb), cudaMemcpyDeviceToHost, s));
     KK_CUDA(cudaStreamSynchronize(s));
     if ((int64_t)nb > h->big_cap) return fail(KK_ERR_STATE, "cluster list overflow");
-    std::vector<unsigned long long> packed(total), off(R + 1);
+    std::vector<unsigned long long> packed(total), off_all(nch + 1), off(R + 1);
     if (total) {
         if ((int64_t)total > h->rows_cap) {
             cudaFree(h->rows_buf);
@@ -1220,16 +1229,17 @@ int collect_hist_rows(kk_lattice* h, cudaStream_t s, std::vector<int64_t>& rows)
             KK_CUDA(cudaMalloc(&h->rows_buf, sizeof(unsigned long long) * total));
             h->rows_cap = (int64_t)total;
         }
-        KK_CUDA(launch_hist_emit(h->hist, R, h->row_off, h->rows_buf, s));
+        KK_CUDA(launch_hist_emit(h->hist, R, h->dense, h->row_off, h->rows_buf, s));
         KK_CUDA(cudaMemcpyAsync(packed.data(), h->rows_buf, sizeof(unsigned long long) * total,
                                 cudaMemcpyDeviceToHost, s));
-        KK_CUDA(cudaMemcpyAsync(off.data(), h->row_off, sizeof(unsigned long long) * (R + 1),
+        KK_CUDA(cudaMemcpyAsync(off_all.data(), h->row_off, sizeof(unsigned long long) * (nch + 1),
                                 cudaMemcpyDeviceToHost, s));
     }
     std::vector<unsigned long long> big(2 * nb);
     if (nb)
         KK_CUDA(cudaMemcpyAsync(big.data(), h->big, sizeof(unsigned long long) * 2 * nb, cudaMemcpyDeviceToHost, s));
     KK_CUDA(cudaStreamSynchronize(s));
+    for (int64_t r = 0; r <= R; ++r) off[r] = total ? off_all[r * cpr] : 0ull;
     std::vector<std::pair<int64_t, int64_t>> bigl(nb);
     for (unsigned long long k = 0; k < nb; ++k) bigl[k] = {(int64_t)big[2 * k], (int64_t)big[2 * k + 1]};
     std::sort(bigl.begin(), bigl.end());
@@ -1269,10 +1279,10 @@ int kk_cluster_histogram(kk_handle h, int target, int64_t* out, int64_t capacity
     cudaStream_t s = S(stream);
     int rc = ensure_ccl_workspace(h);
     if (rc != KK_OK) return rc;
-    KK_CUDA(cudaMemsetAsync(h->hist, 0, sizeof(unsigned int) * kDense * h->R, s));
+    KK_CUDA(cudaMemsetAsync(h->hist, 0, sizeof(unsigned int) * h->dense * h->R, s));
     KK_CUDA(cudaMemsetAsync(h->nbig, 0, sizeof(unsigned long long), s));
     KK_CUDA(launch_ccl(h->buf[h->cur], h->g, h->R, target, h->edges, h->node_size, h->node_par, h->node_rep,
-                       h->root_size, h->counter, h->hist, h->big, h->nbig, h->big_cap, s, nullptr));
+                       h->root_size, h->counter, h->hist, h->dense, h->big, h->nbig, h->big_cap, s, nullptr));
     std::vector<int64_t> rows;
     rc = collect_hist_rows(h, s, rows);
     if (rc != KK_OK) return rc;
@@ -1296,11 +1306,11 @@ int kk_cluster_slab(kk_handle h, int target, int64_t* hist_out, int64_t capacity
     cudaStream_t s = S(stream);
     int rc = ensure_ccl_workspace(h);
     if (rc != KK_OK) return rc;
-    KK_CUDA(cudaMemsetAsync(h->hist, 0, sizeof(unsigned int) * kDense, s));
+    KK_CUDA(cudaMemsetAsync(h->hist, 0, sizeof(unsigned int) * h->dense, s));
     KK_CUDA(cudaMemsetAsync(h->nbig, 0, sizeof(unsigned long long), s));
     SlabCclArgs a{h->open_flag, h->compact, open_sizes, h->open_count, open_cap, top_ids, bot_ids};
     KK_CUDA(launch_ccl(h->buf[h->cur], h->g, 1, target, h->edges, h->node_size, h->node_par, h->node_rep,
-                       h->root_size, h->counter, h->hist, h->big, h->nbig, h->big_cap, s, &a));
+                       h->root_size, h->counter, h->hist, h->dense, h->big, h->nbig, h->big_cap, s, &a));
     unsigned int no = 0;
     KK_CUDA(cudaMemcpyAsync(&no, h->open_count, sizeof(no), cudaMemcpyDeviceToHost, s));
     std::vector<int64_t> rows;

@@ -92,7 +92,8 @@ struct CclParams {
     uint32_t* node_rep;            // [node] replica of the node
     unsigned long long* root_size; // [node]
     unsigned int* node_count;      // device counter
-    unsigned int* hist;            // [replica][kDense]
+    unsigned int* hist;            // [replica][dense]
+    int64_t dense;                 // dense histogram bins per replica (sizes below go to hist)
     unsigned long long* big;       // (replica, size) pairs
     unsigned long long* nbig;
     int64_t big_cap;
@@ -106,8 +107,8 @@ struct CclParams {
 };
 
 __device__ __forceinline__ void hist_add(const CclParams& P, int64_t rep, unsigned long long s) {
-    if (s < (unsigned long long)kDense) {
-        atomicAdd(P.hist + rep * kDense + s, 1u);
+    if (s < (unsigned long long)P.dense) {
+        atomicAdd(P.hist + rep * P.dense + s, 1u);
     } else {
         const unsigned long long slot = atomicAdd(P.nbig, 1ull);
         if ((int64_t)slot < P.big_cap) {
@@ -286,7 +287,7 @@ __global__ void __launch_bounds__(kThreads) ccl_tile_kernel(const CclParams P) {
     }
     __syncthreads();
     for (int i = threadIdx.x; i < kSmallHist; i += kThreads)
-        if (shist[i]) atomicAdd(P.hist + rep * kDense + i, shist[i]);
+        if (shist[i]) atomicAdd(P.hist + rep * P.dense + i, shist[i]);
     if (threadIdx.x == 0) node_base = atomicAdd(P.node_count, n_nodes);
     __syncthreads();
     const unsigned int base = node_base;
@@ -474,7 +475,7 @@ int64_t ccl_node_cap(const Geom& g, int64_t replicas) { return ccl_tiles(g, repl
 // (node_cap uint32 each), root_size (node_cap uint64), counter (1 uint32).
 cudaError_t launch_ccl(const uint32_t* lat, const Geom& g, int64_t replicas, int target, uint32_t* edges,
                        uint32_t* node_size, uint32_t* node_par, uint32_t* node_rep,
-                       unsigned long long* root_size, unsigned int* counter, unsigned int* hist,
+                       unsigned long long* root_size, unsigned int* counter, unsigned int* hist, int64_t dense,
                        unsigned long long* big, unsigned long long* nbig, int64_t big_cap, cudaStream_t s,
                        const SlabCclArgs* slab) {
     CclParams P{};
@@ -498,6 +499,7 @@ cudaError_t launch_ccl(const uint32_t* lat, const Geom& g, int64_t replicas, int
     P.root_size = root_size;
     P.node_count = counter;
     P.hist = hist;
+    P.dense = dense;
     P.big = big;
     P.nbig = nbig;
     P.big_cap = big_cap;
@@ -553,13 +555,20 @@ cudaError_t launch_join(int64_t Lx, int64_t nslabs, const uint32_t* top, const u
 }
 
 // ---- dense histogram -> compact rows on the device ------------------------------
-// Per replica r: the nonzero bins (size 1..kDense-1) in size order are written
-// as (size << 32 | count) at row_off[r] ..; row_off = exclusive scan of the
-// per-replica counts.  Three small kernels; the host reads back only the rows.
-__global__ void hist_count_kernel(const unsigned int* hist, unsigned int* rep_rows) {
-    const int64_t r = blockIdx.x;
+// Per replica r and chunk c of kChunk bins: the nonzero bins (size 1 ..
+// dense-1) in size order are written as (size << 32 | count) at
+// row_off[r * nch + c] ..; row_off = exclusive scan of the per-chunk counts.
+// Three small kernels; the host reads back only the rows.
+constexpr int kChunk = 1024;
+
+__global__ void hist_count_kernel(const unsigned int* hist, unsigned int* chunk_rows, int64_t dense) {
+    const int64_t nch = dense / kChunk;
+    const int64_t rc = blockIdx.x, r = rc / nch, c0 = (rc - r * nch) * kChunk;
     unsigned int c = 0;
-    for (int s = threadIdx.x; s < kDense; s += blockDim.x) c += (s > 0 && hist[r * kDense + s]) ? 1u : 0u;
+    for (int s = threadIdx.x; s < kChunk; s += blockDim.x) {
+        const int64_t b = c0 + s;
+        c += (b > 0 && hist[r * dense + b]) ? 1u : 0u;
+    }
     for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
     __shared__ unsigned int part[32];
     if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = c;
@@ -567,7 +576,7 @@ __global__ void hist_count_kernel(const unsigned int* hist, unsigned int* rep_ro
     if (threadIdx.x == 0) {
         unsigned int t = 0;
         for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += part[k];
-        rep_rows[r] = t;
+        chunk_rows[rc] = t;
     }
 }
 
@@ -605,34 +614,40 @@ __global__ void hist_scan_kernel(const unsigned int* rep_rows, unsigned long lon
 }
 
 __global__ void hist_emit_kernel(const unsigned int* hist, const unsigned long long* row_off,
-                                 unsigned long long* rows, int64_t R) {
-    // one warp per replica: bins in order, ballot + popc for the slots
-    const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+                                 unsigned long long* rows, int64_t nchunks, int64_t dense) {
+    // one warp per chunk: bins in order, ballot + popc for the slots
+    const int64_t nch = dense / kChunk;
+    const int64_t rc = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
-    if (r >= R) return;
-    unsigned long long o = row_off[r];
-    for (int s0 = 0; s0 < kDense; s0 += 32) {
-        const int s = s0 + lane;
-        const unsigned int c = s > 0 ? hist[r * kDense + s] : 0u;
+    if (rc >= nchunks) return;
+    const int64_t r = rc / nch, c0 = (rc - r * nch) * kChunk;
+    unsigned long long o = row_off[rc];
+    for (int s0 = 0; s0 < kChunk; s0 += 32) {
+        const int64_t s = c0 + s0 + lane;
+        const unsigned int c = s > 0 ? hist[r * dense + s] : 0u;
         const unsigned int m = __ballot_sync(0xFFFFFFFFu, c != 0u);
         if (c) rows[o + __popc(m & ((1u << lane) - 1u))] = ((unsigned long long)s << 32) | c;
         o += __popc(m);
     }
 }
 
-cudaError_t launch_hist_compact(const unsigned int* hist, int64_t R, unsigned int* rep_rows,
+int64_t hist_chunks(int64_t R, int64_t dense) { return R * (dense / kChunk); }
+
+cudaError_t launch_hist_compact(const unsigned int* hist, int64_t R, int64_t dense, unsigned int* chunk_rows,
                                 unsigned long long* row_off, cudaStream_t s) {
-    hist_count_kernel<<<(unsigned)R, 256, 0, s>>>(hist, rep_rows);
-    hist_scan_kernel<<<1, 1024, 0, s>>>(rep_rows, row_off, R);
+    const int64_t n = hist_chunks(R, dense);
+    hist_count_kernel<<<(unsigned)n, 256, 0, s>>>(hist, chunk_rows, dense);
+    hist_scan_kernel<<<1, 1024, 0, s>>>(chunk_rows, row_off, n);
     count_launch();
     count_launch();
     return cudaGetLastError();
 }
 
-cudaError_t launch_hist_emit(const unsigned int* hist, int64_t R, const unsigned long long* row_off,
+cudaError_t launch_hist_emit(const unsigned int* hist, int64_t R, int64_t dense, const unsigned long long* row_off,
                              unsigned long long* rows, cudaStream_t s) {
-    const unsigned gx = (unsigned)((R + 7) / 8);
-    hist_emit_kernel<<<gx, 256, 0, s>>>(hist, row_off, rows, R);
+    const int64_t n = hist_chunks(R, dense);
+    const unsigned gx = (unsigned)((n + 7) / 8);
+    hist_emit_kernel<<<gx, 256, 0, s>>>(hist, row_off, rows, n, dense);
     count_launch();
     return cudaGetLastError();
 }
