@@ -132,7 +132,6 @@ struct PassParams {
     int32_t vec_wb;            // write-back with 16-byte vectors (W % 4 == 0, TWI % 4 == 0, no tail)
     int32_t mt_off, wm_off, rl_off, th_off, dt_off, red_off;  // shared-memory layout (smem_layout)
     // planar kernel (kk_planar.cu) only
-    int32_t ws_off;            // per-warp draw-queue scratch
     uint32_t thm[4];           // thresholds of |v| = 1..3 on the side that needs a draw (R5)
     int32_t need_dn;           // 1: draws for v < 0 (omega < 0), 0: for v > 0
     int32_t need_any;          // 0: every threshold is 2^32-1 (omega = 0): no draw is ever needed

@@ -935,8 +935,6 @@ __global__ void __launch_bounds__(NT, 1) band_kernel(const BandParams P) {
     int j = P.j0;
     int64_t left = P.n_iters;
     unsigned int gi = 0;  // iterations published
-    const int64_t xrow = (int64_t)W;                 // words per exchanged row
-    const int64_t xside = 3 * xrow, xslot = 2 * xside, xband = 2 * xslot;
 #pragma unroll 1
     while (left > 0) {
         const Words4 sched = philox10(0u, 0u, sweep, ((uint32_t)rep << 8) | kTagSchedule, P.key0, P.key1);

@@ -20,14 +20,12 @@
 //     Z_{d-1}, Y_d, Z_d; with S_c / S_t their A-counts (bit-sliced full
 //     adders), dN_AB = 2 v, v = +-(S_c - S_t) (sign = centre type, R3/R5);
 //   * acceptance (R5): a move with v on the favourable side (dE <= 0) is
-//     accepted without a draw; the others need u32 <= thr[|v|].  Only the
-//     Philox calls that hold a needed uniform are made (each call holds the
-//     uniforms of 4 consecutive centres, R6): the lanes of a warp queue
-//     their needed calls in shared memory and the warp runs the queue
-//     densely, 32 calls per round, each lane comparing its call's 4
-//     uniforms with the three thresholds and OR-ing the results into the
-//     owner's level masks.  Draws are keyed by position (R6), so which calls
-//     are made cannot change any result.
+//     accepted without a draw; the others need u32 <= thr[|v|].  All eight
+//     acceptance calls of the item are made (each holds the uniforms of 4
+//     consecutive centres, R6) and every uniform is compared with the three
+//     thresholds; each centre's |v| picks its result.  (Making only the calls
+//     that hold a needed uniform, through a warp-compacted queue, cost more
+//     than it saved: ~70% of the calls are needed.)
 // Flips are XOR masks per plane word (shared-memory atomics: centres are 4
 // apart, so no write set meets another centre's read set, R4).
 #include <cuda.h>
@@ -105,11 +103,10 @@ __global__ void pack_halo_planar_kernel(const uint4* lat, uint4* top, uint4* bot
 // and G+1 are the one-group halos in x, R8 needs 3T <= 128 columns), then the
 // global group index per tile group, the centre-row table (l | owned << 31),
 // the pair-direction table (uint32 [36*36]: D0 bits of the 4 centres of two
-// pairs at bits 0..3, D1 at 8..11, D2 at 16..19), per-warp scratch for the
-// draw queue (256 u16 tasks, 32 x (counter base, l), 32 x 8 result bytes) and
-// the reduction scratch + TMA barrier.
+// pairs at bits 0..3, D1 at 8..11, D2 at 16..19), the per-iteration table
+// (kx, first centre row, centre rows, j) and the reduction scratch + TMA
+// barrier.
 constexpr int kPad = 32;
-constexpr int kWarpScratch = 0;  // words per warp (no per-warp scratch: the draws are dense per item)
 
 struct PlCtx {
     const uint32_t* rk;
@@ -150,15 +147,13 @@ __device__ __forceinline__ uint32_t mux(uint32_t s, uint32_t a1, uint32_t a0) { 
 __device__ __forceinline__ uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) { return (a & b) | (c & (a | b)); }
 
 // Items of one iteration (class KX, centre rows r_first + 4a, a < nrows), all
-// tile groups.  The loop is CTA-uniform in steps of NT so every warp can run
-// its draw queue with all 32 lanes.
+// tile groups, in rounds of NT items.
 template <int KX, int NT>
 __device__ __forceinline__ void pl_iteration(const PlCtx& X, uint32_t* tile, const uint32_t* gt, const uint32_t* rl,
-                                             const uint32_t* dt, uint32_t* scratch, int G, int Xg0, int Wg,
+                                             const uint32_t* dt, int G, int Xg0, int Wg,
                                              const Walk& wk, int r_first, int nrows, PlAcc& acc) {
     const int WS = X.WS, NG = X.NG;
     const int items = nrows * NG;
-    const int lane = threadIdx.x & 31;
     const int warp_first = (int)(threadIdx.x & ~31u);
     int a = wk.a0, m = wk.w0;
 #pragma unroll 1
@@ -453,7 +448,6 @@ __global__ void __launch_bounds__(NT, 1) planar_pass_kernel(const __grid_constan
     X.mall = P.need_any ? 0xFFFFFFFFu : 0u;
     X.WS = WS;
     X.NG = NG;
-    uint32_t* scratch = pl_smem + P.ws_off + warp * kWarpScratch;
 
     PlAcc acc = {0u, 0u, 0u, 0};
     const Walk wk = make_walk<NT>(NG);
@@ -464,10 +458,10 @@ __global__ void __launch_bounds__(NT, 1) planar_pass_kernel(const __grid_constan
         const int4 it = itab4[t];  // (kx, r_first, nrows, j)
         X.c3 = ((uint32_t)rep << 8) | (uint32_t)it.w;
         switch (it.x) {
-            case 0: pl_iteration<0, NT>(X, tile, gt, rl, dt, scratch, G, Xg0, Wg, wk, it.y, it.z, acc); break;
-            case 1: pl_iteration<1, NT>(X, tile, gt, rl, dt, scratch, G, Xg0, Wg, wk, it.y, it.z, acc); break;
-            case 2: pl_iteration<2, NT>(X, tile, gt, rl, dt, scratch, G, Xg0, Wg, wk, it.y, it.z, acc); break;
-            default: pl_iteration<3, NT>(X, tile, gt, rl, dt, scratch, G, Xg0, Wg, wk, it.y, it.z, acc); break;
+            case 0: pl_iteration<0, NT>(X, tile, gt, rl, dt, G, Xg0, Wg, wk, it.y, it.z, acc); break;
+            case 1: pl_iteration<1, NT>(X, tile, gt, rl, dt, G, Xg0, Wg, wk, it.y, it.z, acc); break;
+            case 2: pl_iteration<2, NT>(X, tile, gt, rl, dt, G, Xg0, Wg, wk, it.y, it.z, acc); break;
+            default: pl_iteration<3, NT>(X, tile, gt, rl, dt, G, Xg0, Wg, wk, it.y, it.z, acc); break;
         }
         __syncthreads();
     }
@@ -529,14 +523,12 @@ int planar_layout(int T, int THI, int TWI, int NT, PassParams* P) {
     const int rl_off = gt_off + NG;
     const int dt_off = rl_off + H;
     const int it_off = (dt_off + 36 * 36 + 3) & ~3;
-    const int ws_off = it_off + 4 * 8;
-    const int red_off = (ws_off + (NT / 32) * kWarpScratch + 1) & ~1;
+    const int red_off = it_off + 4 * 8;
     const int words = red_off + 2 * 4 * 32 + 2;
     if (P) {
         P->mt_off = gt_off;
         P->rl_off = rl_off;
         P->dt_off = dt_off;
-        P->ws_off = ws_off;
         P->red_off = red_off;
         P->wm_off = 0;
         P->th_off = it_off;
