@@ -139,7 +139,24 @@ __device__ __forceinline__ uint32_t run_start(const uint32_t* S, const uint32_t*
 // per-cluster global atomics on a few hot bins serialised in L2).
 constexpr int kSmallHist = 256;
 
+// Phase clocks of the tile kernel (thread 0 of every CTA, summed over CTAs),
+// compiled only with -DKK_CCL_CLK for tools/ccl_clocks.py.
+#ifdef KK_CCL_CLK
+__device__ unsigned long long kk_ccl_clk[16];
+#define KK_CCLK(k)                                                     \
+    if (threadIdx.x == 0) {                                            \
+        const long long c1 = clock64();                                \
+        atomicAdd(&kk_ccl_clk[k], (unsigned long long)(c1 - c0clk));   \
+        c0clk = c1;                                                    \
+    }
+#else
+#define KK_CCLK(k)
+#endif
+
 __global__ void __launch_bounds__(kThreads) ccl_tile_kernel(const CclParams P) {
+#ifdef KK_CCL_CLK
+    long long c0clk = clock64();
+#endif
     extern __shared__ uint32_t smem[];
     uint32_t* tb = smem;                 // [kTR*kTW] target bits
     uint32_t* S = tb + kTR * kTW;        // [kTR*kTW] run-start bits
@@ -174,7 +191,7 @@ __global__ void __launch_bounds__(kThreads) ccl_tile_kernel(const CclParams P) {
         tb[i] = v;
     }
     for (int i = threadIdx.x; i < kSites / 32; i += kThreads) touch[i] = 0;
-    __syncthreads();
+    __syncthreads(); KK_CCLK(0)
     for (int i = threadIdx.x; i < kTR * kTW; i += kThreads) {
         const int w = i % kTW;
         const uint32_t prev = w ? (tb[i - 1] >> 31) : 0u;
@@ -186,7 +203,7 @@ __global__ void __launch_bounds__(kThreads) ccl_tile_kernel(const CclParams P) {
             lab[base + b] = base + b;
         }
     }
-    __syncthreads();
+    __syncthreads(); KK_CCLK(1)
     // run carry per word: the last run start left of the word in its row
     for (int r = threadIdx.x; r < kTR; r += kThreads) {
         uint32_t last = kNone;
@@ -196,7 +213,7 @@ __global__ void __launch_bounds__(kThreads) ccl_tile_kernel(const CclParams P) {
             if (st) last = (uint32_t)(r * kTX + 32 * w + 31 - __clz(st));
         }
     }
-    __syncthreads();
+    __syncthreads(); KK_CCLK(2)
     // unions between runs of rows r and r+1.  The union points of a warp's 32
     // words are compacted into a per-warp list (in the size table's space,
     // unused until the next phase) so that every lane takes one union at a
@@ -245,12 +262,12 @@ __global__ void __launch_bounds__(kThreads) ccl_tile_kernel(const CclParams P) {
             __syncwarp();
         }
     }
-    __syncthreads();
+    __syncthreads(); KK_CCLK(3)
     for (int i = threadIdx.x; i < kTR * kTW; i += kThreads) {
         const int base = (i / kTW) * kTX + 32 * (i % kTW);
         for (uint32_t m = S[i]; m; m &= m - 1) cnt[base + __ffs(m) - 1] = 0;
     }
-    __syncthreads();
+    __syncthreads(); KK_CCLK(4)
     // sizes per root (one atomic per run segment) and edge-touch flags
     for (int i = threadIdx.x; i < kTR * kTW; i += kThreads) {
         const int r = i / kTW, w = i - r * kTW;
@@ -266,7 +283,7 @@ __global__ void __launch_bounds__(kThreads) ccl_tile_kernel(const CclParams P) {
             if (edge_row || x0 == 0 || x1 == w_tile - 1) atomicOr(&touch[root >> 5], 1u << (root & 31));
         }
     }
-    __syncthreads();
+    __syncthreads(); KK_CCLK(5)
     // complete components -> histogram; edge components -> local node index
     for (int i = threadIdx.x; i < kTR * kTW; i += kThreads) {
         const int base = (i / kTW) * kTX + 32 * (i % kTW);
@@ -285,11 +302,11 @@ __global__ void __launch_bounds__(kThreads) ccl_tile_kernel(const CclParams P) {
             }
         }
     }
-    __syncthreads();
+    __syncthreads(); KK_CCLK(6)
     for (int i = threadIdx.x; i < kSmallHist; i += kThreads)
         if (shist[i]) atomicAdd(P.hist + rep * P.dense + i, shist[i]);
     if (threadIdx.x == 0) node_base = atomicAdd(P.node_count, n_nodes);
-    __syncthreads();
+    __syncthreads(); KK_CCLK(7)
     const unsigned int base = node_base;
     for (unsigned int k = threadIdx.x; k < n_nodes; k += kThreads) {
         if ((int64_t)(base + k) < P.node_cap) {
@@ -313,6 +330,7 @@ __global__ void __launch_bounds__(kThreads) ccl_tile_kernel(const CclParams P) {
             v = base + cnt[root_of(lab, run_start(S, C, r, x))];
         E[e] = v;
     }
+    KK_CCLK(8)
 }
 
 // ---- phase 2: unions across tile boundaries -----------------------------------
@@ -461,6 +479,15 @@ int grid_for_n(int64_t n) {
 }
 
 }  // namespace
+
+#ifdef KK_CCL_CLK
+extern "C" int kk_debug_ccl_clocks(unsigned long long* out) {
+    cudaMemcpyFromSymbol(out, kk_ccl_clk, sizeof(kk_ccl_clk));
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(kk_ccl_clk, z, sizeof(z));
+    return 0;
+}
+#endif
 
 // Workspace sizes for launch_ccl (bytes), given the geometry and replicas.
 int64_t ccl_tiles(const Geom& g, int64_t replicas) {
