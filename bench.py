@@ -174,6 +174,23 @@ def kernel_counters(plan: dict):
     return cnt, None
 
 
+def philox_floor(upd_rate: float):
+    """The R6 Philox work as a time floor: 3 Philox4x32-10 calls per 8 centres
+    at the rate Philox rounds alone reach on this GPU (tools/philox_rate.cu, 4
+    interleaved streams, 768-thread CTAs, one per SM; committed in
+    profiles/r02_philox_rate.txt) — the pass cannot beat it whatever else it
+    overlaps.  None if the measurement is not in the tree."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_philox_rate.txt")) as f:
+            line = next(ln for ln in f if ln.startswith("wide") and "N=4" in ln and "threads= 768" in ln)
+        calls = float(line.split(":")[1].split("G calls/s")[0]) * 1e9
+    except Exception:  # noqa: BLE001
+        return None
+    bound = calls * 8.0 / 3.0
+    return {"calls_per_update": 3.0 / 8.0, "philox_calls_per_s": calls, "bound_updates_per_s": bound,
+            "frac": upd_rate / bound, "source": "tools/philox_rate.cu; profiles/r02_philox_rate.txt"}
+
+
 # ------------------------------------------------------------------------ CPU baseline
 def cpu_baseline(seconds: float, omega: float, fraction: float, seed: int):
     """The oracle as it stands (single-threaded C), on a bounded sample."""
@@ -370,6 +387,7 @@ def measure(ctx, rows, scaling, with_e2e=True):
                      "ops_source": cnt.get("source")})
     else:
         roof.update({"achieved": None, "frac": None, "traffic": None, "note": why})
+    roof["philox_floor"] = philox_floor(upd_rate)
     roof["share_of_step"] = float(np.sum(pass_ms)) / (ms / 1.0) if ms > 0 else None
     roof["hbm"] = {"achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s",
                    "frac": hbm_achieved / hbm_peak, "bytes_per_launch": hbm_bytes_per_launch,

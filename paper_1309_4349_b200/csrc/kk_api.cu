@@ -317,6 +317,8 @@ void set_slab_bands(kk_lattice* h) {
 // (tools/planar_tune.py): 128 x 356 609 G/s, 128 x 276 598, 128 x 200 577,
 // 64 x 596 578, 64 x 444 553, 32 x 996 529 — wide tiles (fewer halo groups)
 // and tall ones (fewer waves) both pay.  KK_TWI / KK_THI force the targets.
+// CTA size 768 (80 registers, no spills): 65536^2 667 G/s vs 658 at 640 and
+// 656 at 896 (896 spills 12 bytes); 16384^2 586 vs 566; 4096^2 296 vs 295.
 void choose_tiles_planar(kk_lattice* h, int nsm) {
     const int T = h->T, NT = h->pass_nt;
     const int twi_env = env_int("KK_TWI", 0), thi_env = env_int("KK_THI", 0);
@@ -809,7 +811,7 @@ int plan_handle(kk_lattice* h, const kk_config* c, int T, int nsm) {
     h->planar = planar_ok && !h->cluster_size && !h->nbands;
     if (h->planar) {
         const int forced = env_int("KK_PASS_THREADS", 0);
-        h->pass_nt = (forced == 512 || forced == 640 || forced == 768 || forced == 896) ? forced : 640;
+        h->pass_nt = (forced == 512 || forced == 640 || forced == 768 || forced == 896) ? forced : 768;
         choose_tiles_planar(h, nsm);
         set_slab_bands(h);
         const int64_t ctas = (int64_t)h->tiles_x * h->bands * h->R;

@@ -32,7 +32,7 @@ def test_bench_lattice_plan(monkeypatch):
     assert p["tile_words"] == 128 and 300 <= p["tile_rows"] <= 400   # widest TMA tile, as tall as fits
     assert p["smem_bytes"] <= 227 * 1024 and p["tma_boxes"] >= 1
     assert p["ctas"] == p["tiles_x"] * p["bands"] >= 148 * 16
-    assert p["threads"] == 640
+    assert p["threads"] == 768
     assert p["pass_pdl"] == 0                       # early CTAs would idle in slots
     # the row-major tile kernel's plan (KK_PLANAR=0; every lattice with Lx % 128 != 0)
     monkeypatch.setenv("KK_PLANAR", "0")
