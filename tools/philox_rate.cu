@@ -4,7 +4,9 @@
 // prints calls/s, thread-instructions/s (40 per call: 20 IMAD.WIDE + 20 LOP3)
 // and the fraction of the 128 lane-ops/clk/SM issue peak; "+k x 4 LOP3" adds
 // independent 3-input logic per stream-round (can it fill the idle slots?).  Variants: the
-// 64-bit product (IMAD.WIDE.U32) and the split __umulhi + low multiply.
+// 64-bit product (IMAD.WIDE.U32) and the split __umulhi + low multiply; round
+// keys from the constant bank (as in the pass kernel), as immediates, or in
+// ordinary registers.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/philox_rate tools/philox_rate.cu
 #include <cstdint>
 #include <cstdio>
@@ -13,9 +15,16 @@
 constexpr uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
 __constant__ uint32_t rk[20];
 
-template <int N, bool SPLIT, int EXTRA = 0>
+template <int N, bool SPLIT, int EXTRA = 0, int KEYS = 0>
 __global__ void __launch_bounds__(768, 1) philox_kernel(int K, uint32_t* out) {
     uint32_t acc = 0;
+    uint32_t kr[20];
+#pragma unroll
+    for (int r = 0; r < 20; ++r) {
+        if (KEYS == 1) kr[r] = 0x1234u + (r % 10) * 0x9E3779B9u + (r / 10) * 0x4444u;
+        else if (KEYS == 2) kr[r] = __shfl_sync(0xFFFFFFFFu, rk[r] + (threadIdx.x & 1u), 0);  // in ordinary registers
+        else kr[r] = rk[r];
+    }
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t x0 = t * 3u, x1 = t ^ 0x55u, x2 = t + 9u, x3 = ~t;  // independent LOP3 work (EXTRA per stream-round)
 #pragma unroll 1
@@ -45,7 +54,7 @@ __global__ void __launch_bounds__(768, 1) philox_kernel(int K, uint32_t* out) {
                     h1 = (uint32_t)(p1 >> 32);
                     l1 = (uint32_t)p1;
                 }
-                const uint32_t na = h1 ^ b[p] ^ rk[r], nc = h0 ^ d[p] ^ rk[10 + r];
+                const uint32_t na = h1 ^ b[p] ^ kr[r], nc = h0 ^ d[p] ^ kr[10 + r];
 #pragma unroll
                 for (int e = 0; e < EXTRA; ++e) {
                     x0 = (x0 & x1) ^ x2;
@@ -65,17 +74,17 @@ __global__ void __launch_bounds__(768, 1) philox_kernel(int K, uint32_t* out) {
     if ((acc ^ x0 ^ x1 ^ x2 ^ x3) == 0x12345678u) out[t] = acc;
 }
 
-template <int N, bool SPLIT, int EXTRA = 0>
+template <int N, bool SPLIT, int EXTRA = 0, int KEYS = 0>
 void run(int threads, int ctas, const char* name) {
     uint32_t* out;
     cudaMalloc(&out, (size_t)threads * ctas * 4);
     const int K = 2000;
-    philox_kernel<N, SPLIT, EXTRA><<<ctas, threads>>>(10, out);
+    philox_kernel<N, SPLIT, EXTRA, KEYS><<<ctas, threads>>>(10, out);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    philox_kernel<N, SPLIT, EXTRA><<<ctas, threads>>>(K, out);
+    philox_kernel<N, SPLIT, EXTRA, KEYS><<<ctas, threads>>>(K, out);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms = 0;
@@ -109,6 +118,8 @@ int main() {
         run<1, false>(th, nsm, "wide");
         run<4, false, 1>(th, nsm, "wide+lop");
         run<4, false, 2>(th, nsm, "wide+lop");
+        run<4, false, 0, 1>(th, nsm, "keys-imm");
+        run<4, false, 0, 2>(th, nsm, "keys-reg");
     }
     return 0;
 }
