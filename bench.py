@@ -175,7 +175,7 @@ def kernel_counters(plan: dict):
 
 
 def philox_floor(upd_rate: float):
-    """The R6 Philox work as a time floor: 3 Philox4x32-10 calls per 8 centres
+    """The R6 Philox work as a time floor: 2 Philox4x32-10 calls per 8 centres
     at the rate Philox rounds alone reach on this GPU (tools/philox_rate.cu, 4
     interleaved streams, 768-thread CTAs, one per SM; committed in
     profiles/r02_philox_rate.txt) — the pass cannot beat it whatever else it
@@ -186,8 +186,8 @@ def philox_floor(upd_rate: float):
         calls = float(line.split(":")[1].split("G calls/s")[0]) * 1e9
     except Exception:  # noqa: BLE001
         return None
-    bound = calls * 8.0 / 3.0
-    return {"calls_per_update": 3.0 / 8.0, "philox_calls_per_s": calls, "bound_updates_per_s": bound,
+    bound = calls * 4.0
+    return {"calls_per_update": 1.0 / 4.0, "philox_calls_per_s": calls, "bound_updates_per_s": bound,
             "frac": upd_rate / bound, "source": "tools/philox_rate.cu; profiles/r02_philox_rate.txt"}
 
 
@@ -366,9 +366,10 @@ def measure(ctx, rows, scaling, with_e2e=True):
     peak_src = f"{n_sm} SMs x 128 lanes x {sm_max_mhz:.0f} MHz (max SM clock, {peak_src})"
     upd_rate = upd_per_launch / pass_avg_s
     # implementation-independent floor: the Philox work R6
-    # fixes (3 Philox4x32-10 calls per 8 centres, 10 rounds x 2 wide
-    # multiplies + 2 three-way XORs = 40 integer ops a call: 15 ops / update)
-    floor = 15.0
+    # fixes (2 Philox4x32-10 calls per 8 centres, 10 rounds x 2 wide
+    # multiplies + 2 three-way XORs = 40 integer ops a call: 10 ops / update,
+    # plus the one multiply that splits each centre's word into d and u: 11)
+    floor = 11.0
     roof = {"bound": "alu", "unit": "Tlane-op/s", "peak": alu_peak, "peak_source": peak_src,
             "kernel": kname, "plan": {k: plan[k] for k in ("kernel", "tile_words", "tile_rows", "threads",
                                                           "tma_boxes", "ctas")},

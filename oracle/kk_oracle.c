@@ -257,11 +257,11 @@ void kko_schedule(uint64_t seed, uint32_t sweep, uint32_t replica, int ks[16]) {
 /* Random draws of centre (x,y) in iteration j of sweep s (reading R6):
  * centre index i = (x - kx)/4 along its row, octet g = i >> 3 (8 consecutive
  * centres), position p = i & 7, centre row l = (y - ky)/4; with
- * c3 = replica<<8 | j:
- *   direction: q = floor(philox(4g, l, s, c3)[p >> 1] * 36 / 2^32) encodes the
- *     directions of the centre pair (p & ~1, p | 1): d = q / 6 for the even
- *     position, d = q % 6 for the odd one (each uniform on 0..5 to 36/2^32);
- *   acceptance: u32 = philox(4g + 1 + (p >> 2), l, s, c3)[p & 3]. */
+ * c3 = replica<<8 | j, the centre's word is
+ *   w = philox(2g + (p >> 2), l, s, c3)[p & 3]
+ * and 6 w = d 2^32 + u32 splits it into the direction d = floor(6 w / 2^32)
+ * (uniform on 0..5 to 6/2^32) and the acceptance uniform u32 = 6 w mod 2^32
+ * (given d, uniform on a step-6 progression of [0, 2^32)). */
 void kko_center_draw(uint64_t seed, uint32_t sweep, uint32_t replica, int j,
                      int kx, int ky, int64_t x, int64_t y, int* d, uint32_t* u32) {
     int64_t i = (x - kx) / 4, l = (y - ky) / 4;
@@ -269,11 +269,10 @@ void kko_center_draw(uint64_t seed, uint32_t sweep, uint32_t replica, int j,
     int p = (int)(i & 7);
     uint32_t c3 = (replica << 8) | (uint32_t)j;
     uint32_t w[4];
-    philox_seeded((uint32_t)(4 * g), (uint32_t)l, sweep, c3, seed, w);
-    uint32_t q = (uint32_t)(((uint64_t)w[p >> 1] * 36u) >> 32);
-    *d = (p & 1) ? (int)(q % 6u) : (int)(q / 6u);
-    philox_seeded((uint32_t)(4 * g + 1 + (p >> 2)), (uint32_t)l, sweep, c3, seed, w);
-    *u32 = w[p & 3];
+    philox_seeded((uint32_t)(2 * g + (p >> 2)), (uint32_t)l, sweep, c3, seed, w);
+    uint64_t six_w = (uint64_t)w[p & 3] * 6u;
+    *d = (int)(six_w >> 32);
+    *u32 = (uint32_t)six_w;
 }
 
 /* One MPKK sweep = one Monte Carlo step: 16 iterations;

@@ -180,7 +180,7 @@ struct BandParams {
 // Shared-memory layout of the pass and resident kernels (word offsets): the
 // tile (H rows x WS words) at 0, then the per-pass tables — centre-octet
 // table (uint2 [Wt]), ownership masks ([Wt]), centre-row table ([H]), pair
-// threshold table (uint2 [256]), pair direction table (uint16 [36*36]) — and
+// threshold table (uint2 [256]), direction table (uint16 [36*36]) — and
 // the reduction scratch ([4][16] uint64 + a TMA barrier).  Computed on the
 // host and passed in the kernel parameters, so every table base is a
 // constant-bank operand in the inner loop.

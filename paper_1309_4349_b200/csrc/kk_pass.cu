@@ -111,14 +111,15 @@ struct Tabs {
     int wm_off;                // uint32 [Wt]: owned bits of the word (0 for halo words)
     int rl_off;                // uint32 [H]: centre-row index l | owned-row flag << 31
     int th_off;                // uint2 [256]: thresholds of the two nibbles of a byte of idx
-    int dt_off;                // uint16 [36*36]: direction nibbles of two centre pairs from (q_a, q_b)
+    int dt_off;                // uint16 [36*36]: direction nibbles of four centres from (6 d0 + d1, 6 d2 + d3)
     uint32_t Lx;
     int WS;
     int rW, rTail, rRows;      // resident kernel: lattice words, Lx % 32, rows (tile kernel: unused)
 };
 
-// Pair direction table (R6): entry qa*36 + qb = the direction nibbles of two
-// centre pairs, byte 0 = (qa/6) | (qa%6) << 4, byte 1 likewise for qb.
+// Direction table (R6): entry qa*36 + qb = the direction nibbles of four
+// centres (qa = 6 d0 + d1, qb = 6 d2 + d3): byte 0 = d0 | d1 << 4, byte 1 =
+// d2 | d3 << 4.
 template <int NT>
 __device__ __forceinline__ void fill_dir_table(const Tabs& S) {
     uint16_t* dt = reinterpret_cast<uint16_t*>(kk_smem + S.dt_off);
@@ -143,43 +144,42 @@ __device__ __forceinline__ void process_item(const Tabs& S, int r, int w, uint32
     const uint32_t rl = kk_smem[S.rl_off + r];
     const uint32_t l = rl & 0x7FFFFFFFu;
     const uint2 mq = reinterpret_cast<const uint2*>(kk_smem + S.mt_off)[w];
-    // ---- random draws (R6): octet g of 8 centres; call 4g gives the four
-    // pair-direction words (q = w*36 >> 32 -> d_even = q/6, d_odd = q%6),
-    // calls 4g+1, 4g+2 the eight acceptance uniforms.
+    // ---- random draws (R6): octet g of 8 centres; calls 2g, 2g+1 give one
+    // word w per centre (centre p: call 2g + (p >> 2), word p & 3), split as
+    // 6 w = d 2^32 + u: direction d, acceptance uniform u.
     // FAST: the octet draws have no branch around them, so they and the SWAR
     // neighbourhood work below form one basic block the scheduler can
     // interleave (Philox is IMAD-heavy, the SWAR part LOP3/SHF-heavy).
     uint32_t u[8];
     uint32_t dv = 0;  // direction nibble vector: nibble q = direction of centre q
+    const uint16_t* dt = reinterpret_cast<const uint16_t*>(kk_smem + S.dt_off);
     if (FAST || mq.y) {  // the word is one whole octet (common case)
-        const uint32_t g4 = (mq.x >> 5) * 4u;
-        const uint32_t m[3] = {g4, g4 + 1u, g4 + 2u};
-        uint32_t R3[3][4];
-        philox10_xn<3>(m, l, sweep, c3, rk, R3);
+        const uint32_t g2 = (mq.x >> 5) * 2u;
+        const uint32_t m[2] = {g2, g2 + 1u};
+        uint32_t R2[2][4];
+        philox10_xn<2>(m, l, sweep, c3, rk, R2);
+        uint32_t d[8];
 #pragma unroll
-        for (int p = 0; p < 4; ++p) {
-            u[p] = R3[1][p];
-            u[4 + p] = R3[2][p];
+        for (int p = 0; p < 8; ++p) {
+            const uint64_t six_w = (uint64_t)R2[p >> 2][p & 3] * 6u;
+            d[p] = (uint32_t)(six_w >> 32);
+            u[p] = (uint32_t)six_w;
         }
-        // pair p's direction word w gives q = w*36 >> 32 in [0, 36): d = q/6 for
-        // the even centre, q%6 for the odd one; two pairs per table lookup
-        const uint16_t* dt = reinterpret_cast<const uint16_t*>(kk_smem + S.dt_off);
-        const uint32_t q0 = __umulhi(R3[0][0], 36u), q1 = __umulhi(R3[0][1], 36u);
-        const uint32_t q2 = __umulhi(R3[0][2], 36u), q3 = __umulhi(R3[0][3], 36u);
-        dv = (uint32_t)dt[q0 * 36u + q1] | ((uint32_t)dt[q2 * 36u + q3] << 16);
+        // four directions per table lookup: entry (6 d0 + d1) * 36 + 6 d2 + d3
+        dv = (uint32_t)dt[((d[0] * 6u + d[1]) * 6u + d[2]) * 6u + d[3]] |
+             ((uint32_t)dt[((d[4] * 6u + d[5]) * 6u + d[6]) * 6u + d[7]] << 16);
     } else {  // word straddles an octet boundary (x wrap, Lx % 32 != 0, tiny Lx)
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
             uint32_t x = mq.x + 4u * q + KX;
             while (x >= S.Lx) x -= S.Lx;
-            const uint32_t i = (x - KX) >> 2, g4 = (i >> 3) * 4u, pos = i & 7u;
-            const uint32_t m2[2] = {g4, g4 + 1u + (pos >> 2)};
-            uint32_t R2[2][4];
-            philox10_xn<2>(m2, l, sweep, c3, rk, R2);
-            const uint32_t qq = __umulhi(sel4(R2[0], pos >> 1), 36u);
-            const uint32_t de = (qq * 43u) >> 8;
-            dv |= ((pos & 1u) ? (qq - 6u * de) : de) << (4 * q);
-            u[q] = sel4(R2[1], pos & 3u);
+            const uint32_t i = (x - KX) >> 2, pos = i & 7u;
+            const uint32_t m1[1] = {(i >> 3) * 2u + (pos >> 2)};
+            uint32_t R1[1][4];
+            philox10_xn<1>(m1, l, sweep, c3, rk, R1);
+            const uint64_t six_w = (uint64_t)sel4(R1[0], pos & 3u) * 6u;
+            dv |= (uint32_t)(six_w >> 32) << (4 * q);
+            u[q] = (uint32_t)six_w;
         }
     }
 

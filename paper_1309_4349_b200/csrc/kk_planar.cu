@@ -19,13 +19,15 @@
 //     neighbours n_{d+2..d+4} and the partner's exclusive neighbours
 //     Z_{d-1}, Y_d, Z_d; with S_c / S_t their A-counts (bit-sliced full
 //     adders), dN_AB = 2 v, v = +-(S_c - S_t) (sign = centre type, R3/R5);
+//   * draws (R6): eight Philox calls per item, one 32-bit word w per centre,
+//     split as 6 w = d 2^32 + u into the direction d and the acceptance
+//     uniform u (one 32x32->64 multiply);
 //   * acceptance (R5): a move with v on the favourable side (dE <= 0) is
-//     accepted without a draw; the others need u32 <= thr[|v|].  All eight
-//     acceptance calls of the item are made (each holds the uniforms of 4
-//     consecutive centres, R6) and every uniform is compared with the three
-//     thresholds; each centre's |v| picks its result.  (Making only the calls
-//     that hold a needed uniform, through a warp-compacted queue, cost more
-//     than it saved: ~70% of the calls are needed.)
+//     accepted without a draw; the others need u <= thr[|v|].  Every uniform
+//     is compared with the three thresholds as soon as it is drawn; each
+//     centre's |v| picks its result.  (Comparing only the uniforms that are
+//     needed, through a warp-compacted queue, cost more than it saved: ~70%
+//     of the calls are needed.)
 // Flips are XOR masks per plane word (shared-memory atomics: centres are 4
 // apart, so no write set meets another centre's read set, R4).
 #include <cuda.h>
@@ -102,8 +104,8 @@ __global__ void pack_halo_planar_kernel(const uint4* lat, uint4* top, uint4* bot
 // tile row 0 land here), the tile (H rows x WS = 4 (G + 2) words: tile group 0
 // and G+1 are the one-group halos in x, R8 needs 3T <= 128 columns), then the
 // global group index per tile group, the centre-row table (l | owned << 31),
-// the pair-direction table (uint32 [36*36]: D0 bits of the 4 centres of two
-// pairs at bits 0..3, D1 at 8..11, D2 at 16..19), the per-iteration table
+// the direction table (uint32 [36*36], entry (6 d0 + d1) * 36 + 6 d2 + d3: D0
+// bits of the 4 centres at bits 0..3, D1 at 8..11, D2 at 16..19), the per-iteration table
 // (kx, first centre row, centre rows, j) and the reduction scratch + TMA
 // barrier.
 constexpr int kPad = 32;
@@ -167,19 +169,39 @@ __device__ __forceinline__ void pl_iteration(const PlCtx& X, uint32_t* tile, con
             rlw = rl[r];
             l = rlw & 0x7FFFFFFFu;
             Mg = gt[m];
-            // ---- direction draws (R6): call 4g for octet g = 4 Mg + o, word k2 = pair k2
-            uint32_t R4[4][4];
-            {
-                const uint32_t c0 = 16u * Mg;
-                const uint32_t mm[4] = {c0, c0 + 4u, c0 + 8u, c0 + 12u};
-                philox10_xn<4>(mm, l, X.sweep, X.c3, X.rk, R4);
-            }
+            // ---- draws (R6): call c = 8 Mg + q (q = 0..7, octet g = 4 Mg + (q >> 1))
+            // holds the words of centres 4q..4q+3; 6 w = d 2^32 + u gives the
+            // direction d and the acceptance uniform u.  Every uniform is tested
+            // against the thresholds of |v| = 1, 2, 3 here (R5: L1..L3), before
+            // the energy change is known; each centre's |v| picks its result
+            // below.  Four directions per table lookup (entry (6 d0 + d1) * 36 +
+            // 6 d2 + d3), transposed into the bit planes D0..D2.
+            uint32_t L1 = 0, L2 = 0, L3 = 0;
             uint32_t f[4];
 #pragma unroll
-            for (int o = 0; o < 4; ++o) {
-                const uint32_t ea = dt[__umulhi(R4[o][0], 36u) * 36u + __umulhi(R4[o][1], 36u)];
-                const uint32_t eb = dt[__umulhi(R4[o][2], 36u) * 36u + __umulhi(R4[o][3], 36u)];
-                f[o] = ea + (eb << 4);  // byte 0 = D0 of the octet's 8 centres, byte 1 = D1, byte 2 = D2
+            for (int bt = 0; bt < 2; ++bt) {
+                const uint32_t c0 = 8u * Mg + 4u * bt;
+                const uint32_t mm[4] = {c0, c0 + 1u, c0 + 2u, c0 + 3u};
+                uint32_t U[4][4];
+                philox10_xn<4>(mm, l, X.sweep, X.c3, X.rk, U);
+                uint32_t e[4];
+#pragma unroll
+                for (int qd = 0; qd < 4; ++qd) {
+                    uint32_t d[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const uint64_t pr = (uint64_t)U[qd][i] * 6u;
+                        d[i] = (uint32_t)(pr >> 32);
+                        const uint32_t u = (uint32_t)pr;
+                        const uint32_t bit = 1u << (16 * bt + 4 * qd + i);
+                        L1 = or_if_le(L1, u, X.t1, bit);
+                        L2 = or_if_le(L2, u, X.t2, bit);
+                        L3 = or_if_le(L3, u, X.t3, bit);
+                    }
+                    e[qd] = dt[((d[0] * 6u + d[1]) * 6u + d[2]) * 6u + d[3]];
+                }
+                f[2 * bt] = e[0] + (e[1] << 4);
+                f[2 * bt + 1] = e[2] + (e[3] << 4);
             }
             {
                 const uint32_t lo01 = __byte_perm(f[0], f[1], 0x5140), lo23 = __byte_perm(f[2], f[3], 0x5140);
@@ -257,31 +279,7 @@ __device__ __forceinline__ void pl_iteration(const PlCtx& X, uint32_t* tile, con
             dn = mux(C, ltm, gtm);  // v < 0
             need = nontriv & mux(X.mdn, dn, up) & X.mall;
             autoacc = nontriv & ~need;
-            // ---- acceptance draws (R6): call 4g + 1 + h holds the uniforms of
-            // quad k = 2 (g - 4 Mg) + h (centres 4k..4k+3); all eight calls of
-            // the item, in two batches of four interleaved streams.  Each
-            // uniform is tested against the thresholds of |v| = 1, 2, 3 (R5)
-            // and the centre's own |v| picks the result.  (Skipping the
-            // |v| = 2, 3 tests warp-uniformly when no centre needs them was
-            // measured slower: 609 vs 657 G/s on 65536^2.)
-            uint32_t L1 = 0, L2 = 0, L3 = 0;
-#pragma unroll
-            for (int bt = 0; bt < 2; ++bt) {
-                const uint32_t c0 = 16u * Mg + 1u + 8u * bt;
-                const uint32_t mm[4] = {c0, c0 + 1u, c0 + 4u, c0 + 5u};
-                uint32_t U[4][4];
-                philox10_xn<4>(mm, l, X.sweep, X.c3, X.rk, U);
-#pragma unroll
-                for (int qd = 0; qd < 4; ++qd) {
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const uint32_t bit = 1u << (16 * bt + 4 * qd + i);
-                        L1 = or_if_le(L1, U[qd][i], X.t1, bit);
-                        L2 = or_if_le(L2, U[qd][i], X.t2, bit);
-                        L3 = or_if_le(L3, U[qd][i], X.t3, bit);
-                    }
-                }
-            }
+            // accepted with a draw: u <= thr[|v|] (R5)
             drawn = need & mux(M1, mux(M0, L3, L2), L1);
         }
         if (has) {
@@ -369,7 +367,7 @@ __global__ void __launch_bounds__(NT, 1) planar_pass_kernel(const __grid_constan
             tma_load_3d(smem_u32(tile + y0 * WS), &tmap, tma_bar, 4 * gx0, (int)(Y0 - HY + y0), rep);
         }
     }
-    // pair-direction table (R6): entry qa*36 + qb, centres 0..3 = (qa/6, qa%6, qb/6, qb%6)
+    // direction table (R6): entry qa*36 + qb, centres 0..3 = (qa/6, qa%6, qb/6, qb%6)
     for (int i = threadIdx.x; i < 36 * 36; i += NT) {
         const uint32_t qa = (uint32_t)i / 36u, qb = (uint32_t)i % 36u;
         const uint32_t d[4] = {qa / 6u, qa % 6u, qb / 6u, qb % 6u};

@@ -4,6 +4,7 @@ Pinned against (a) the Random123 known-answer vectors (tests/golden) and
 (b) an independent implementation: Triton's numpy interpreter of
 ``tl.randint4x`` (counter = (offset, 0, 0, 0), key = (seed lo, seed hi)).
 """
+import math
 import os
 import subprocess
 import sys
@@ -66,9 +67,9 @@ def test_philox_matches_triton_interpreter(seed):
 
 def test_schedule_and_draw_layout():
     """k_j are the 16 nibbles of words 0,1 of philox((0,0,s,tag 0x10)); the
-    centre draw (reading R6) takes the pair's direction word from
-    philox(4g, l, s, c3)[p>>1] split as q = w*36>>32 -> (q/6, q%6) and u32
-    from philox(4g+1+(p>>2), l, s, c3)[p&3] — checked against Philox."""
+    centre draw (reading R6) takes the centre's word w from
+    philox(2g+(p>>2), l, s, c3)[p&3] and splits 6 w = d 2^32 + u32 into the
+    direction d and the acceptance uniform u32 — checked against Philox."""
     seed, s = 987654321, 17
     key = (seed & 0xFFFFFFFF, seed >> 32)
     w = O.philox4x32_10((0, 0, s, 0x10), key)
@@ -79,9 +80,32 @@ def test_schedule_and_draw_layout():
         i, l = (x - kx) // 4, (y - ky) // 4
         g, p = i >> 3, i & 7
         c3 = (2 << 8) | j
-        q = (O.philox4x32_10((4 * g, l, s, c3), key)[p >> 1] * 36) >> 32
-        u = O.philox4x32_10((4 * g + 1 + (p >> 2), l, s, c3), key)[p & 3]
+        ww = O.philox4x32_10((2 * g + (p >> 2), l, s, c3), key)[p & 3]
         d, uu = O.center_draw(seed, s, 2, j, kx, ky, x, y)
-        assert d == (q % 6 if p & 1 else q // 6)
-        assert uu == u
-        assert 0 <= d < 6
+        assert d == (6 * ww) >> 32 and 0 <= d < 6
+        assert uu == (6 * ww) % 2 ** 32
+
+
+@pytest.mark.parametrize("omega", [0.2, 0.5, 0.6, 1.0, 2.5])
+def test_split_word_acceptance_is_boltzmann_for_every_direction(omega):
+    """R6's split 6 w = d 2^32 + u32 of a uniform 32-bit w: for every direction
+    d the probability that u32 passes the acceptance rule (u32 2^-32 <
+    exp(-dE)) is exp(-dE) to within 8 * 2^-32 — so the acceptance law does not
+    depend on the proposed direction (detailed balance).
+    Counted exactly: the w of class d are the integers in [d 2^32 / 6,
+    (d+1) 2^32 / 6), and u32 = 6 w - d 2^32 steps by 6 over them."""
+    two32 = 2 ** 32
+    for dn in [2, 4, 6]:
+        pe = math.exp(-omega * dn)
+        for d in range(6):
+            lo = -(-d * two32 // 6)            # first w of class d
+            hi = -(-(d + 1) * two32 // 6)      # first w of class d + 1
+            u0 = 6 * lo - d * two32            # its u32 (0, 2 or 4)
+            # accepted w: u0 + 6 k < pe 2^32 (the oracle's rule, in exact arithmetic up to fp64 of pe)
+            lim = pe * two32
+            k_max = math.ceil((lim - u0) / 6)  # number of k >= 0 with u0 + 6k < lim
+            n_acc = max(0, min(hi - lo, k_max))
+            assert abs(n_acc / (hi - lo) - pe) <= 8 / two32
+            # and the oracle's own rule agrees at the boundary of that count
+            assert O.metropolis_accept(omega * dn, u0 + 6 * (n_acc - 1))
+            assert not O.metropolis_accept(omega * dn, u0 + 6 * n_acc)
