@@ -171,7 +171,20 @@ def kernel_counters(plan: dict):
     got = cnt.get("plan", {})
     if any(got.get(k) != v for k, v in want.items()):
         return None, f"counters captured for plan {got}, this run uses {want}"
+    if cnt.get("source_sha256") != pass_source_sha256():
+        return None, "counters captured from different pass-kernel sources"
     return cnt, None
+
+
+def pass_source_sha256():
+    """Fingerprint of the pass-kernel sources the counters describe (the
+    capture is refused after any change to them)."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in ("kk_planar.cu", "kk_pass.cu", "kk_device.cuh", "kk_internal.cuh"):
+        with open(os.path.join(ROOT, "paper_1309_4349_b200", "csrc", f), "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()
 
 
 def philox_floor(upd_rate: float):
@@ -384,6 +397,7 @@ def measure(ctx, rows, scaling, with_e2e=True):
                      "per_launch_ops": lane_ops, "thread_inst_per_update": cnt["thread_inst_per_update"],
                      "alu_pipe_frac": cnt.get("alu_pipe_pct", 0) / 100.0,
                      "fma_pipe_frac": cnt.get("fma_pipe_pct", 0) / 100.0,
+                     "fmaheavy_pipe_frac": cnt.get("fmaheavy_pipe_pct", 0) / 100.0,
                      "issue_active_frac": cnt.get("issue_active_pct", 0) / 100.0,
                      "ops_source": cnt.get("source")})
     else:

@@ -353,6 +353,11 @@ void choose_tiles_planar(kk_lattice* h, int nsm) {
                 work += rounds + 0.3 * (std::ceil(rounds) - rounds);
             }
             work += 0.05 * (double)(h->THI + 6 * T) * NG / NT + 1.0;  // staging (TMA) + fixed
+            // the two halo groups cost more than their item count (fitted on
+            // B200 after the R6 revision: 4096^2 32 x 112 326 vs 64 x 56 345,
+            // 8192^2 64 x 224 555 vs 128 x 112 574, 16384^2 64 x 444 640 vs
+            // 128 x 224 666 G/s)
+            work *= 1.0 + 1.33 / NG;
             const int64_t ctas = (int64_t)h->tiles_x * h->bands * h->R;
             const double t = (double)((ctas + nsm - 1) / nsm) * work;
             if (t < best * 0.999) {
@@ -815,6 +820,11 @@ int plan_handle(kk_lattice* h, const kk_config* c, int T, int nsm) {
         choose_tiles_planar(h, nsm);
         set_slab_bands(h);
         const int64_t ctas = (int64_t)h->tiles_x * h->bands * h->R;
+        // one-wave grids whose largest iteration has <= 512 items: 512-thread
+        // CTAs (4096^2, 64 x 56 tiles: 352 vs 345 G/s at 768 threads)
+        if (!forced && ctas <= (int64_t)nsm &&
+            (int64_t)((h->THI + 3 * (T - 1) + 2 + 3) / 4) * (h->TWI / 4 + 2) <= 512)
+            h->pass_nt = 512;
         const int pdl = env_int("KK_PDL", -1);
         h->pass_pdl = pdl < 0 ? ctas <= (int64_t)nsm : pdl != 0;
         if (planar_layout(T, h->THI, h->TWI, h->pass_nt, nullptr) > 227 * 1024)

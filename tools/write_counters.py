@@ -12,6 +12,7 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1309_4349_b200 import kk  # noqa: E402
+import bench  # noqa: E402
 
 rep, upd, tile = sys.argv[1], float(sys.argv[2]), sys.argv[3]
 out = sys.argv[4] if len(sys.argv) > 4 else os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
@@ -37,9 +38,11 @@ d = {
     "issue_active_pct": round(val("smsp__issue_active.avg.pct_of_peak_sustained_active"), 2),
     "alu_pipe_pct": round(val("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"), 2),
     "fma_pipe_pct": round(val("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"), 2),
+    "fmaheavy_pipe_pct": round(val("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed"), 2),
     "source": os.environ.get("KK_COUNTERS_SOURCE", f"ncu --set full --clock-control none of the bench lattice; "
                                                     f"{os.path.basename(rep)}"),
     "tile": tile,
+    "source_sha256": bench.pass_source_sha256(),
     "plan": {k: v for k, v in kk.plan(65536, 65536, iters_per_pass=8, n_sm=148).items()
              if k in ("kernel", "iters_per_pass", "tile_words", "tile_rows", "threads", "tma_boxes")},
 }
