@@ -20,6 +20,8 @@
 // Global traffic is one bit per site plus the tile edges, instead of a
 // 4-8 byte label per site.  The resulting multiset is unique, so the output
 // does not depend on scheduling.
+#include <cstdlib>
+
 #include "kk_internal.cuh"
 
 namespace kk {
@@ -333,6 +335,255 @@ __global__ void __launch_bounds__(kThreads) ccl_tile_kernel(const CclParams P) {
     KK_CCLK(8)
 }
 
+// ---- phase 1 (run-id variant, the default): union-find over compact run ids --
+// Runs get consecutive ids in row-major order: with B = the number of run
+// starts before a word (a CTA scan of popc(S)), the run containing target
+// site x (bit b of word w, row r) is
+//     id = B[r, w] + popc(S[r, w] & bits 0..b) - 1,
+// which also covers a run entering the word from the left (popc = 0).  Rows r
+// and r+1 are bonded by (0,+1) and (+1,+1): site x of row r+1 touches x and
+// x-1 of row r, so one union per overlapping run pair suffices — at the
+// positions of O = t1 & (t0 | t0 << 1) where O starts, a run of row r+1
+// starts, or the attached run of row r changes (a run start of row r).  Sizes
+// are summed per run (no contention), then per root with one aggregated
+// atomic per warp and root.
+constexpr int kWords = kTR * kTW;
+constexpr int kMaxRuns = kSites / 2;
+
+__device__ __forceinline__ uint32_t mask_le(int b) { return 0xFFFFFFFFu >> (31 - b); }
+
+// Union of the trees of nodes a and b (any members, e.g. a root found by an
+// earlier union): both walks interleaved (path splitting), then the larger
+// root is linked under the smaller by CAS.  Returns the surviving root.
+__device__ __forceinline__ uint32_t union_nodes(uint32_t* par, uint32_t a, uint32_t b) {
+    volatile uint32_t* vp = par;
+    for (;;) {
+        uint32_t pa = vp[a], pb = vp[b];
+        while (pa != a || pb != b) {
+            if (pa != a) {
+                const uint32_t ga = vp[pa];
+                if (ga != pa) vp[a] = ga;
+                a = pa;
+                pa = ga;
+            }
+            if (pb != b) {
+                const uint32_t gb = vp[pb];
+                if (gb != pb) vp[b] = gb;
+                b = pb;
+                pb = gb;
+            }
+        }
+        if (a == b) return a;
+        const uint32_t hi = a > b ? a : b, lo = a > b ? b : a;
+        const uint32_t old = atomicCAS(par + hi, hi, lo);
+        if (old == hi) return lo;
+        a = old;  // hi was linked meanwhile: continue from its new parent
+        b = lo;
+    }
+}
+
+// Exclusive scan of c over the CTA in thread order (two barriers); total =
+// the sum.  wsum: kThreads / 32 + 1 words of shared scratch.
+__device__ __forceinline__ uint32_t cta_excl_scan(uint32_t c, uint32_t* wsum, uint32_t& total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t x = lane < kThreads / 32 ? wsum[lane] : 0u;
+        uint32_t xi = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, xi, o);
+            if (lane >= o) xi += t;
+        }
+        if (lane < kThreads / 32) wsum[lane] = xi - x;
+        if (lane == kThreads / 32 - 1) wsum[kThreads / 32] = xi;
+    }
+    __syncthreads();
+    total = wsum[kThreads / 32];
+    return wsum[warp] + incl - c;
+}
+
+__global__ void __launch_bounds__(kThreads) ccl_runs_kernel(const CclParams P) {
+#ifdef KK_CCL_CLK
+    long long c0clk = clock64();
+#endif
+    extern __shared__ uint32_t smem[];
+    uint32_t* tb = smem;                   // [kWords] target bits
+    uint32_t* S = tb + kWords;             // [kWords] run starts
+    uint32_t* B = S + kWords;              // [kWords] runs started before the word
+    uint32_t* par = B + kWords;            // [kMaxRuns] union-find parent of each run
+    uint32_t* rsz = par + kMaxRuns;        // [kMaxRuns] run size; root: component size, then node index
+    uint32_t* touch = rsz + kMaxRuns;      // [kMaxRuns / 32] run / component touches the tile edge
+    uint16_t* node_s = reinterpret_cast<uint16_t*>(touch + kMaxRuns / 32);  // [kEdge]
+    __shared__ unsigned int n_nodes, node_base;
+    __shared__ unsigned int wsum[kThreads / 32 + 1];
+    __shared__ unsigned int shist[kSmallHist];
+
+    const Geom& g = P.g;
+    const int tx = blockIdx.x, ty = blockIdx.y;
+    const int64_t rep = blockIdx.z;
+    const int64_t X0 = (int64_t)tx * kTX, Y0 = (int64_t)ty * kTR;
+    const int w_tile = (int)min64(kTX, g.Lx - X0);
+    const int h_tile = (int)min64(kTR, g.rows - Y0);
+    const uint32_t* lat = P.lat + rep * g.rep_words;
+    const uint32_t tmask = P.target ? 0u : 0xFFFFFFFFu;
+    const int i = threadIdx.x, lane = i & 31, warp = i >> 5;
+    const int r = i / kTW, w = i - r * kTW;
+
+    if (i == 0) n_nodes = 0;
+    for (int k = i; k < kSmallHist; k += kThreads) shist[k] = 0u;
+    for (int k = i; k < kMaxRuns / 32; k += kThreads) touch[k] = 0u;
+    // ---- load, run starts, run ids
+    uint32_t v = 0;
+    if (r < h_tile && 32 * w < w_tile) {
+        v = lat[(Y0 + r) * g.W + X0 / 32 + w] ^ tmask;  // 1 = target site
+        const int nv = w_tile - 32 * w;
+        if (nv < 32) v &= (1u << nv) - 1u;
+    }
+    const uint32_t vl = __shfl_up_sync(0xFFFFFFFFu, v, 1);  // left word of the row (kTW divides 32)
+    const uint32_t st = v & ~((v << 1) | (w ? vl >> 31 : 0u));
+    const uint32_t c = __popc(st);
+    uint32_t nr;
+    const uint32_t b0 = cta_excl_scan(c, wsum, nr);
+    tb[i] = v;
+    S[i] = st;
+    B[i] = b0;
+    for (uint32_t k = i; k < nr; k += kThreads) par[k] = k;
+    __syncthreads(); KK_CCLK(0)
+    // ---- unions between rows r-1 and r (this thread's word is in row r).
+    // The union points of the tile are listed in thread order (idc << 16 |
+    // ida, in the run-size array, unused until the next phase) and split into
+    // equal contiguous shares, so no warp waits for one with a dense row
+    // block; consecutive points often share a run, whose root is reused.
+    uint32_t U = 0, t0 = 0, s0 = 0, bb0 = 0;
+    if (r >= 1 && r < h_tile) {
+        t0 = tb[i - kTW];
+        s0 = S[i - kTW];
+        bb0 = B[i - kTW];
+        const uint32_t t0l = w ? tb[i - kTW - 1] : 0u;
+        const uint32_t tp = t0 | (t0 << 1) | (t0l >> 31);
+        const uint32_t O = v & tp;
+        const uint32_t ocarry = w ? ((vl >> 31) & ((t0l >> 31) | (t0l >> 30)) & 1u) : 0u;
+        U = O & ~(((O << 1) | ocarry) & ~st & ~s0);
+    }
+    uint32_t nu;
+    uint32_t k = cta_excl_scan(__popc(U), wsum, nu);
+    uint32_t last_c = 0xFFFFFFFFu, last_a = 0xFFFFFFFFu, root = 0;
+    if (nu <= (uint32_t)kMaxRuns) {
+        while (U) {
+            const int b = __ffs(U) - 1;
+            U &= U - 1;
+            const uint32_t m = mask_le(b);
+            const uint32_t idc = b0 + __popc(st & m) - 1;
+            const uint32_t ma = ((t0 >> b) & 1u) ? m : (m >> 1);
+            rsz[k++] = (idc << 16) | (bb0 + __popc(s0 & ma) - 1);
+        }
+        __syncthreads();
+        const uint32_t e1 = (uint32_t)(((uint64_t)nu * (i + 1)) / kThreads);
+        for (uint32_t e = (uint32_t)(((uint64_t)nu * i) / kThreads); e < e1; ++e) {
+            const uint32_t pr = rsz[e], idc = pr >> 16, ida = pr & 0xFFFFu;
+            root = union_nodes(par, idc == last_c ? root : idc, ida == last_a ? root : ida);
+            last_c = idc;
+            last_a = ida;
+        }
+    } else {  // more points than list space (a near-checkerboard tile): each thread its own
+        while (U) {
+            const int b = __ffs(U) - 1;
+            U &= U - 1;
+            const uint32_t m = mask_le(b);
+            const uint32_t idc = b0 + __popc(st & m) - 1;
+            const uint32_t ma = ((t0 >> b) & 1u) ? m : (m >> 1);
+            const uint32_t ida = bb0 + __popc(s0 & ma) - 1;
+            root = union_nodes(par, idc == last_c ? root : idc, ida == last_a ? root : ida);
+            last_c = idc;
+            last_a = ida;
+        }
+    }
+    __syncthreads();
+    for (uint32_t q = i; q < nr; q += kThreads) rsz[q] = 0u;
+    __syncthreads();
+    KK_CCLK(1)
+    // ---- run sizes (per run segment of the word) and edge touches
+    {
+        const bool edge_row = (r == 0 || r == h_tile - 1);
+        for (uint32_t m = v; m;) {
+            const uint64_t M = m, Lb = M & (~M + 1);
+            const uint32_t seg = (uint32_t)(((M + Lb) ^ M) & M);
+            m &= ~seg;
+            const int xb0 = __ffs(seg) - 1;
+            const int xb1 = 31 - __clz(seg);
+            const uint32_t id = b0 + __popc(st & mask_le(xb0)) - 1;
+            atomicAdd(&rsz[id], (uint32_t)__popc(seg));
+            if (edge_row || (w == 0 && xb0 == 0) || 32 * w + xb1 == w_tile - 1) atomicOr(&touch[id >> 5], 1u << (id & 31));
+        }
+    }
+    __syncthreads(); KK_CCLK(2)
+    // ---- component sizes and edge touches at the roots
+    for (uint32_t k = i; k < nr; k += kThreads) {
+        const uint32_t root = find32(par, k);
+        if (root != k) {
+            atomicAdd(&rsz[root], rsz[k]);
+            if ((touch[k >> 5] >> (k & 31)) & 1u) atomicOr(&touch[root >> 5], 1u << (root & 31));
+        }
+    }
+    __syncthreads(); KK_CCLK(3)
+    // ---- complete components -> histogram; edge components -> local node index
+    for (uint32_t k = i; k < nr; k += kThreads) {
+        if (par[k] != k) continue;
+        const uint32_t sz = rsz[k];
+        if ((touch[k >> 5] >> (k & 31)) & 1u) {
+            const unsigned int n = atomicAdd(&n_nodes, 1u);
+            node_s[n] = (uint16_t)sz;
+            rsz[k] = n;
+        } else if (sz < kSmallHist) {
+            atomicAdd(&shist[sz], 1u);
+        } else {
+            hist_add(P, rep, sz);
+        }
+    }
+    __syncthreads(); KK_CCLK(4)
+    for (int k = i; k < kSmallHist; k += kThreads)
+        if (shist[k]) atomicAdd(P.hist + rep * P.dense + k, shist[k]);
+    if (i == 0) node_base = atomicAdd(P.node_count, n_nodes);
+    __syncthreads();
+    const unsigned int base = node_base;
+    for (unsigned int k = i; k < n_nodes; k += kThreads) {
+        if ((int64_t)(base + k) < P.node_cap) {
+            P.node_size[base + k] = node_s[k];
+            P.node_par[base + k] = base + k;
+            P.node_rep[base + k] = (uint32_t)rep;
+            P.root_size[base + k] = 0ull;
+        }
+    }
+    // ---- edge export: node id of every target edge site
+    const int64_t tile = (rep * P.tiles_y + ty) * P.tiles_x + tx;
+    uint32_t* E = P.edges + tile * kEdge;
+    for (int e = i; e < kEdge; e += kThreads) {
+        int er, ex;
+        if (e < kTX) { er = 0; ex = e; }
+        else if (e < 2 * kTX) { er = h_tile - 1; ex = e - kTX; }
+        else if (e < 2 * kTX + kTR) { er = e - 2 * kTX; ex = 0; }
+        else { er = e - 2 * kTX - kTR; ex = w_tile - 1; }
+        uint32_t val = kNone;
+        if (er < h_tile && ex < w_tile) {
+            const int wi = er * kTW + (ex >> 5);
+            if ((tb[wi] >> (ex & 31)) & 1u) {
+                const uint32_t id = B[wi] + __popc(S[wi] & mask_le(ex & 31)) - 1;
+                val = base + rsz[root_of(par, id)];
+            }
+        }
+        E[e] = val;
+    }
+    KK_CCLK(5)
+}
+
 // ---- phase 2: unions across tile boundaries -----------------------------------
 __global__ void ccl_merge_kernel(const CclParams P) {
     const Geom& g = P.g;
@@ -505,6 +756,10 @@ cudaError_t launch_ccl(const uint32_t* lat, const Geom& g, int64_t replicas, int
                        unsigned long long* root_size, unsigned int* counter, unsigned int* hist, int64_t dense,
                        unsigned long long* big, unsigned long long* nbig, int64_t big_cap, cudaStream_t s,
                        const SlabCclArgs* slab) {
+    static const bool ccl_old_tiles = [] {
+        const char* v = std::getenv("KK_CCL_OLD");
+        return v && *v == '1';
+    }();
     CclParams P{};
     P.periodic_y = slab ? 0 : 1;
     if (slab) {
@@ -533,10 +788,17 @@ cudaError_t launch_ccl(const uint32_t* lat, const Geom& g, int64_t replicas, int
     P.node_cap = ccl_node_cap(g, replicas);
     cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(unsigned int), s);
     if (e != cudaSuccess) return e;
-    const int smem = 4 * (2 * kTR * kTW + kSites / 32 + kSites + kSites / 2 + kEdge / 2 + kTR * kTW);
-    e = ensure_dynamic_smem((const void*)ccl_tile_kernel, smem);
-    if (e != cudaSuccess) return e;
-    ccl_tile_kernel<<<dim3(P.tiles_x, P.tiles_y, (unsigned)replicas), kThreads, smem, s>>>(P);
+    if (ccl_old_tiles) {
+        const int smem = 4 * (2 * kTR * kTW + kSites / 32 + kSites + kSites / 2 + kEdge / 2 + kTR * kTW);
+        e = ensure_dynamic_smem((const void*)ccl_tile_kernel, smem);
+        if (e != cudaSuccess) return e;
+        ccl_tile_kernel<<<dim3(P.tiles_x, P.tiles_y, (unsigned)replicas), kThreads, smem, s>>>(P);
+    } else {
+        const int smem = 4 * (3 * kWords + 2 * kMaxRuns + kMaxRuns / 32 + kEdge / 2);
+        e = ensure_dynamic_smem((const void*)ccl_runs_kernel, smem);
+        if (e != cudaSuccess) return e;
+        ccl_runs_kernel<<<dim3(P.tiles_x, P.tiles_y, (unsigned)replicas), kThreads, smem, s>>>(P);
+    }
     count_launch();
     const int64_t per_rep = (int64_t)P.tiles_x * P.tiles_y * (kTR + kTX);
     int bx = grid_for_n(per_rep);
