@@ -628,11 +628,32 @@ __global__ void ccl_merge_kernel(const CclParams P) {
 }
 
 // ---- phase 3: flatten + sum sizes per root, then histogram roots ----------------
+// Consecutive nodes (one tile's, in creation order) often share a root (the
+// percolating cluster's above all): the lanes of a warp sum runs of equal
+// roots first (segmented shuffle scan) so a root gets one 64-bit atomic per
+// run instead of one per node.
 __global__ void ccl_nodes_sum_kernel(const CclParams P) {
     const unsigned int n = (unsigned int)min64((int64_t)*P.node_count, P.node_cap);
-    for (unsigned int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const uint32_t r = find32(P.node_par, i);
-        atomicAdd(P.root_size + r, (unsigned long long)P.node_size[i]);
+    const int lane = threadIdx.x & 31;
+    const unsigned int stride = gridDim.x * blockDim.x;
+    for (unsigned int i0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); i0 < n; i0 += stride) {
+        const unsigned int i = i0 + lane;
+        const bool ok = i < n;
+        const uint32_t r = ok ? find32(P.node_par, i) : 0xFFFFFFFFu;
+        uint32_t v = ok ? P.node_size[i] : 0u;
+        const uint32_t rp = __shfl_up_sync(0xFFFFFFFFu, r, 1);
+        const uint32_t rn = __shfl_down_sync(0xFFFFFFFFu, r, 1);
+        const bool head = lane == 0 || rp != r;
+        const bool tail = lane == 31 || rn != r;
+        // segmented inclusive scan: lane l adds lane l - o while no head lies between
+        uint32_t hb = __ballot_sync(0xFFFFFFFFu, head);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, v, o);
+            const uint32_t between = (hb >> (lane - o + 1)) & ((1u << o) - 1u);  // heads in (lane-o, lane]
+            if (lane >= o && !between) v += t;
+        }
+        if (ok && tail) atomicAdd(P.root_size + r, (unsigned long long)v);
     }
 }
 
