@@ -5,17 +5,17 @@
 // label merging.  On the GPU the lattice is cut into tiles (kTR rows x
 // kTW words) and the cluster multiset is built in three phases:
 //
-//  1. tile kernel (shared memory): load the tile's bits, union-find over the
-//     six-neighbour bonds that stay inside the tile (32-bit labels, shared
-//     memory CAS), count each local component's size.  Components that touch no
-//     tile edge are complete: their sizes go straight into the histogram.
-//     Edge-touching components become global "nodes" (size recorded) and the
-//     tile writes the node id of every edge site.
+//  1. tile kernel (shared memory, ccl_runs_kernel): load the tile's bits,
+//     give every row run a compact id, union-find over the runs joined by the
+//     bonds that stay inside the tile, sum each local component's size.
+//     Components that touch no tile edge are complete: their sizes go
+//     straight into the histogram.  Edge-touching components become global
+//     "nodes" (size recorded) and the tile writes the node id of every edge
+//     site.
 //  2. merge kernel: for every bond crossing a tile boundary (periodic
 //     lattice), union the two nodes in a global union-find (CAS linking of the
 //     larger root under the smaller).
-//  3. node kernels: flatten, sum node sizes per root (64-bit), histogram the
-//     roots.
+//  3. node kernels: sum node sizes per root (64-bit), histogram the roots.
 //
 // Global traffic is one bit per site plus the tile edges, instead of a
 // 4-8 byte label per site.  The resulting multiset is unique, so the output
@@ -34,13 +34,11 @@ namespace {
 constexpr int kTR = KK_CCL_ROWS;           // tile rows
 constexpr int kTW = 8;                     // tile words per row (256 sites)
 constexpr int kTX = 32 * kTW;              // tile sites per row
-constexpr int kSites = kTR * kTX;          // 16384 (16-bit local sizes)
+constexpr int kSites = kTR * kTX;          // 16384 (16-bit node sizes, run ids)
 constexpr int kEdge = 2 * kTX + 2 * kTR;   // edge entries per tile
 constexpr int kThreads = kTR * kTW;  // one thread per tile word in the per-word phases
 static_assert(kSites <= 65535 && kThreads <= 1024, "16-bit local sizes, one thread per tile word");
 constexpr uint32_t kNone = 0xFFFFFFFFu;
-// 32-bit labels in shared memory: sub-word CAS is emulated by a CAS loop on the
-// containing word, which races with the plain 16-bit stores of path halving.
 
 __device__ __forceinline__ uint32_t find32(uint32_t* par, uint32_t v) {
     volatile uint32_t* vp = par;
