@@ -83,12 +83,14 @@ struct Acc {
     uint32_t attempted, trivial, accepted;
     uint32_t idx_even, idx_odd;  // byte-lane sums of (v+3) over accepted centres (flushed every 32 items)
     unsigned long long idx_sum;
+    uint32_t pend;               // items since the last flush (band_iteration)
 };
 
 __device__ __forceinline__ void acc_flush(Acc& a) {
     a.idx_sum += ((a.idx_even & 0x00FF00FFu) + ((a.idx_even >> 8) & 0x00FF00FFu)) * 0x00010001u >> 16;
     a.idx_sum += ((a.idx_odd & 0x00FF00FFu) + ((a.idx_odd >> 8) & 0x00FF00FFu)) * 0x00010001u >> 16;
     a.idx_even = a.idx_odd = 0u;
+    a.pend = 0u;
 }
 
 
@@ -855,14 +857,10 @@ __device__ __forceinline__ void band_iteration(const Tabs& S, const Walk& wk, in
     int a = wk.a0;
     int w = wk.w0;
     const int da = wk.da, dw = wk.dw;
-    int since_flush = 0;
     for (int it = threadIdx.x; it < items; it += NT) {
         const int r = a < n1 ? r1 + 4 * a : r2 + 4 * (a - n1);
         process_item<KX, 2, true>(S, r, w + 1, sweep, c3, rk, acc);
-        if (++since_flush == 32) {
-            acc_flush(acc);
-            since_flush = 0;
-        }
+        if (++acc.pend == 32) acc_flush(acc);  // counted across calls: no flush per iteration
         a += da;
         w += dw;
         if (w >= W) {
@@ -1081,6 +1079,11 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) cluster_kernel(const Ba
     S.dt_off = P.dt_off;
     const Walk wk = make_walk<NT>(W), wk2 = make_walk<NT>(W + 2);
     unsigned long long* red = reinterpret_cast<unsigned long long*>(kk_smem + P.red_off);
+    // per-block iteration table (kx | j << 8, first centre row, centre rows,
+    // sweep) in the unused part of the reduction scratch (NT <= 512: the
+    // counters take <= 128 of its 256 words)
+    int4* itab = reinterpret_cast<int4*>(kk_smem + ((P.red_off + 128 + 3) & ~3));  // 16-byte aligned
+    static_assert(L2X || (NT <= 512 && TB <= 8), "iteration table fits the reduction scratch");
     uint2* thr2 = reinterpret_cast<uint2*>(kk_smem + S.th_off);
     uint2* mtab = reinterpret_cast<uint2*>(kk_smem + S.mt_off);
     for (int i = threadIdx.x; i < 256; i += NT) thr2[i] = make_uint2(P.thr[min(i & 15, 6)], P.thr[min(i >> 4, 6)]);
@@ -1129,11 +1132,11 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) cluster_kernel(const Ba
             sa = philox10(0u, 0u, sweep, ((uint32_t)rep << 8) | kTagSchedule, P.key0, P.key1);
             sb = j + tb > 16 ? philox10(0u, 0u, sweep + 1u, ((uint32_t)rep << 8) | kTagSchedule, P.key0, P.key1)
                              : sa;
-        } else {
+        } else if (threadIdx.x < TB) {
             // class, rows of the exact light cone of the block's remaining
-            // iterations, sweep and c3 per iteration, computed here with
-            // compile-time indices so the arrays stay in registers (a runtime
-            // index in the loop below would put them in local memory)
+            // iterations, sweep and c3 of iteration t = threadIdx.x, into the
+            // shared iteration table (the other threads only read it: this
+            // per-block setup is not repeated by all 256 threads)
             uint32_t s2 = sweep;
             int j2 = j;
             Words4 sc = philox10(0u, 0u, s2, ((uint32_t)rep << 8) | kTagSchedule, P.key0, P.key1);
@@ -1167,7 +1170,12 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) cluster_kernel(const Ba
                 rf[t] = r_lo + ((ph - r_lo) & 3);
                 nr[t] = r_hi > rf[t] ? (r_hi - rf[t] + 3) / 4 : 0;
             }
+#pragma unroll
+            for (int t = 0; t < TB; ++t)
+                if (t == (int)threadIdx.x)
+                    itab[t] = make_int4((int)(ks[t] | ((uint32_t)js[t] << 8)), rf[t], nr[t], (int)sw[t]);
         }
+        if constexpr (!L2X) __syncthreads();
 #pragma unroll 1
         for (int t = 0; t < tb; ++t) {
             uint32_t kst, swt;
@@ -1198,20 +1206,12 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) cluster_kernel(const Ba
                 r_first = r_lo + ((ph - r_lo) & 3);
                 nrows = r_hi > r_first ? (r_hi - r_first + 3) / 4 : 0;
             } else {
-                kst = ks[0];
-                swt = sw[0];
-                jst = js[0];
-                r_first = rf[0];
-                nrows = nr[0];
-#pragma unroll
-                for (int u = 1; u < TB; ++u)
-                    if (t == u) {
-                        kst = ks[u];
-                        swt = sw[u];
-                        jst = js[u];
-                        r_first = rf[u];
-                        nrows = nr[u];
-                    }
+                const int4 it = itab[t];
+                kst = (uint32_t)it.x & 15u;
+                jst = it.x >> 8;
+                r_first = it.y;
+                nrows = it.z;
+                swt = (uint32_t)it.w;
             }
             const int kx = (int)(kst & 3u);
             const uint32_t c3 = ((uint32_t)rep << 8) | (uint32_t)jst;
@@ -1224,7 +1224,6 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) cluster_kernel(const Ba
                 case 2: band_iteration<2, NT>(S, wi, r_first, nrows, 0, 0, swt, c3, P.rk, acc); break;
                 default: band_iteration<3, NT>(S, wi, r_first, nrows, 0, 0, swt, c3, P.rk, acc); break;
             }
-            acc_flush(acc);
             __syncthreads();
             band_refresh<NT>(S, H);
             __syncthreads();
@@ -1236,6 +1235,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) cluster_kernel(const Ba
         }
         left -= tb;
         // counters of this block (<= TB iterations: 32-bit sums per warp cannot overflow)
+        acc_flush(acc);
         {
             uint32_t c0 = acc.attempted, c1 = acc.trivial, c2 = acc.accepted, c3s = (uint32_t)acc.idx_sum;
 #pragma unroll
