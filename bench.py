@@ -171,17 +171,19 @@ def kernel_counters(plan: dict):
     got = cnt.get("plan", {})
     if any(got.get(k) != v for k, v in want.items()):
         return None, f"counters captured for plan {got}, this run uses {want}"
-    if cnt.get("source_sha256") != pass_source_sha256():
+    if cnt.get("source_sha256") != pass_source_sha256(plan["kernel"]):
         return None, "counters captured from different pass-kernel sources"
     return cnt, None
 
 
-def pass_source_sha256():
-    """Fingerprint of the pass-kernel sources the counters describe (the
-    capture is refused after any change to them)."""
+def pass_source_sha256(kernel: str = "planar"):
+    """Fingerprint of the sources of the pass kernel the counters describe
+    (the capture is refused after any change to them)."""
     import hashlib
-    h = hashlib.sha256()
-    for f in ("kk_planar.cu", "kk_pass.cu", "kk_device.cuh", "kk_internal.cuh"):
+    files = {"planar": ("kk_planar.cu", "kk_device.cuh", "kk_internal.cuh"),
+             "tile": ("kk_pass.cu", "kk_device.cuh", "kk_internal.cuh")}.get(kernel, ())
+    h = hashlib.sha256(kernel.encode())
+    for f in files:
         with open(os.path.join(ROOT, "paper_1309_4349_b200", "csrc", f), "rb") as fh:
             h.update(fh.read())
     return h.hexdigest()

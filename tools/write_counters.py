@@ -42,7 +42,7 @@ d = {
     "source": os.environ.get("KK_COUNTERS_SOURCE", f"ncu --set full --clock-control none of the bench lattice; "
                                                     f"{os.path.basename(rep)}"),
     "tile": tile,
-    "source_sha256": bench.pass_source_sha256(),
+    "source_sha256": bench.pass_source_sha256(kk.plan(65536, 65536, iters_per_pass=8, n_sm=148)["kernel"]),
     "plan": {k: v for k, v in kk.plan(65536, 65536, iters_per_pass=8, n_sm=148).items()
              if k in ("kernel", "iters_per_pass", "tile_words", "tile_rows", "threads", "tma_boxes")},
 }
