@@ -160,6 +160,10 @@ class GpuSlab:
         """Full periodic lattice: [(size, count)] of replica 0."""
         return self.lat.cluster_histogram(target, stream=stream)[0]
 
+    def cluster_histogram_array(self, target, stream):
+        """As cluster_histogram_rows, as an (n, 2) int64 array (no per-row Python objects)."""
+        return self.lat.cluster_histogram_raw(target, stream=stream)[:, 1:]
+
     # slab cluster histogram (multi-GPU)
     def alloc_cluster_buffers(self):
         t = self.torch
@@ -291,10 +295,12 @@ class SlabDriver:
         out = {"n_ab": nab.tolist(), "n_a": na.tolist(), "attempted": st[:, 0].tolist(),
                "trivial": st[:, 1].tolist(), "accepted": st[:, 2].tolist(), "dnab_sum": st[:, 3].tolist()}
         if ccl:
-            h = self.cluster_histogram(1)
+            h = (self.be.cluster_histogram_array(1, self.stream) if self.world == 1 and
+                 hasattr(self.be, "cluster_histogram_array") else self.cluster_histogram(1))
             if h is not None:
-                out["clusters_A"] = int(sum(c for _, c in h))
-                out["largest_A"] = int(max((sz for sz, _ in h), default=0))
+                h = np.asarray(h, np.int64).reshape(-1, 2)
+                out["clusters_A"] = int(h[:, 1].sum())
+                out["largest_A"] = int(h[:, 0].max()) if len(h) else 0
         return out
 
 

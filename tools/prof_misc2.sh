@@ -1,0 +1,4 @@
+cd $GRAFT_REPO_ROOT
+python tools/ccl_overhead.py > gpurun_out/ccl_overhead.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:planar_pass -s 60 -c 1 -f -o gpurun_out/r02b_planar_4096 python tools/profile_pass.py 4096 4096 40 8 > gpurun_out/prof_4096.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:ccl_runs -s 1 -c 1 -f -o gpurun_out/r02b_ccl_runs_16384 python tools/profile_ccl.py 16384 100 > gpurun_out/prof_ccl.log 2>&1
