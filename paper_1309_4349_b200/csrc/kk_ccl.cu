@@ -20,8 +20,6 @@
 // Global traffic is one bit per site plus the tile edges, instead of a
 // 4-8 byte label per site.  The resulting multiset is unique, so the output
 // does not depend on scheduling.
-#include <cstdlib>
-
 #include "kk_internal.cuh"
 
 namespace kk {
@@ -29,12 +27,12 @@ namespace kk {
 namespace {
 
 #ifndef KK_CCL_ROWS
-#define KK_CCL_ROWS 64
+#define KK_CCL_ROWS 128  // 128 x 256-site tiles, 1024 threads, two CTAs per SM (64 rows: 19.5 vs 17.5 ms on 65536^2)
 #endif
 constexpr int kTR = KK_CCL_ROWS;           // tile rows
 constexpr int kTW = 8;                     // tile words per row (256 sites)
 constexpr int kTX = 32 * kTW;              // tile sites per row
-constexpr int kSites = kTR * kTX;          // 16384 (16-bit node sizes, run ids)
+constexpr int kSites = kTR * kTX;          // 32768 (16-bit run / component / node sizes)
 constexpr int kEdge = 2 * kTX + 2 * kTR;   // edge entries per tile
 constexpr int kThreads = kTR * kTW;  // one thread per tile word in the per-word phases
 static_assert(kSites <= 65535 && kThreads <= 1024, "16-bit local sizes, one thread per tile word");
@@ -118,22 +116,6 @@ __device__ __forceinline__ void hist_add(const CclParams& P, int64_t rep, unsign
     }
 }
 
-// ---- phase 1: one CTA per tile ------------------------------------------------
-// Row runs: along a row, consecutive target sites are connected by the (+1,0)
-// bond, so each maximal run is labelled by its first site without any union.
-// Union-find then only links runs of neighbouring rows, once per overlapping
-// run pair and bond type ((0,+1) and (+1,+1)): a union point is placed where
-// the overlap starts, i.e. at a run start of either row.
-
-// First site (tile index) of the run containing target site x of row r: the
-// last run start at or below x in x's word, else the carry of the word (the
-// start of the run that enters the word at bit 0, tabulated per word).
-__device__ __forceinline__ uint32_t run_start(const uint32_t* S, const uint32_t* C, int r, int x) {
-    const int wi = x >> 5;
-    const uint32_t m = S[r * kTW + wi] & (0xFFFFFFFFu >> (31 - (x & 31)));
-    return m ? (uint32_t)(r * kTX + 32 * wi + 31 - __clz(m)) : C[r * kTW + wi];
-}
-
 // Cluster sizes below kSmallHist are counted in a per-CTA shared histogram and
 // flushed with one global atomic per nonzero bin (most clusters are small:
 // per-cluster global atomics on a few hot bins serialised in L2).
@@ -153,187 +135,7 @@ __device__ unsigned long long kk_ccl_clk[16];
 #define KK_CCLK(k)
 #endif
 
-__global__ void __launch_bounds__(kThreads) ccl_tile_kernel(const CclParams P) {
-#ifdef KK_CCL_CLK
-    long long c0clk = clock64();
-#endif
-    extern __shared__ uint32_t smem[];
-    uint32_t* tb = smem;                 // [kTR*kTW] target bits
-    uint32_t* S = tb + kTR * kTW;        // [kTR*kTW] run-start bits
-    uint32_t* touch = S + kTR * kTW;     // [kSites/32] edge-touch flag per root
-    uint32_t* lab = touch + kSites / 32; // [kSites] parent of each run start
-    uint32_t* cnt32 = lab + kSites;      // [kSites/2] 16-bit size per root (two per word), then node index
-    uint16_t* cnt = reinterpret_cast<uint16_t*>(cnt32);
-    uint16_t* node_s = reinterpret_cast<uint16_t*>(cnt32 + kSites / 2);  // [kEdge]
-    uint32_t* C = cnt32 + kSites / 2 + kEdge / 2;                         // [kTR*kTW] run carry per word
-    __shared__ unsigned int n_nodes, node_base;
-    __shared__ unsigned int shist[kSmallHist];
-
-    const Geom& g = P.g;
-    const int tx = blockIdx.x, ty = blockIdx.y;
-    const int64_t rep = blockIdx.z;
-    const int64_t X0 = (int64_t)tx * kTX, Y0 = (int64_t)ty * kTR;
-    const int w_tile = (int)min64(kTX, g.Lx - X0);    // valid sites per row
-    const int h_tile = (int)min64(kTR, g.rows - Y0);  // valid rows
-    const uint32_t* lat = P.lat + rep * g.rep_words;
-    const uint32_t tmask = P.target ? 0u : 0xFFFFFFFFu;
-
-    if (threadIdx.x == 0) n_nodes = 0;
-    for (int i = threadIdx.x; i < kSmallHist; i += kThreads) shist[i] = 0u;
-    for (int i = threadIdx.x; i < kTR * kTW; i += kThreads) {
-        const int r = i / kTW, w = i - r * kTW;
-        uint32_t v = 0;
-        if (r < h_tile && 32 * w < w_tile) {
-            v = lat[(Y0 + r) * g.W + X0 / 32 + w] ^ tmask;   // 1 = target site
-            const int nv = w_tile - 32 * w;
-            if (nv < 32) v &= (1u << nv) - 1u;
-        }
-        tb[i] = v;
-    }
-    for (int i = threadIdx.x; i < kSites / 32; i += kThreads) touch[i] = 0;
-    __syncthreads(); KK_CCLK(0)
-    for (int i = threadIdx.x; i < kTR * kTW; i += kThreads) {
-        const int w = i % kTW;
-        const uint32_t prev = w ? (tb[i - 1] >> 31) : 0u;
-        const uint32_t st = tb[i] & ~((tb[i] << 1) | prev);
-        S[i] = st;
-        const int base = (i / kTW) * kTX + 32 * w;
-        for (uint32_t m = st; m; m &= m - 1) {
-            const int b = __ffs(m) - 1;
-            lab[base + b] = base + b;
-        }
-    }
-    __syncthreads(); KK_CCLK(1)
-    // run carry per word: the last run start left of the word in its row
-    for (int r = threadIdx.x; r < kTR; r += kThreads) {
-        uint32_t last = kNone;
-        for (int w = 0; w < kTW; ++w) {
-            C[r * kTW + w] = last;
-            const uint32_t st = S[r * kTW + w];
-            if (st) last = (uint32_t)(r * kTX + 32 * w + 31 - __clz(st));
-        }
-    }
-    __syncthreads(); KK_CCLK(2)
-    // unions between runs of rows r and r+1.  The union points of a warp's 32
-    // words are compacted into a per-warp list (in the size table's space,
-    // unused until the next phase) so that every lane takes one union at a
-    // time instead of looping over its own word's points.
-    {
-        static_assert(kThreads == kTR * kTW, "one thread per tile word");
-        constexpr int kBuf = 256;                       // entries per warp and round
-        const int i = threadIdx.x, lane = i & 31;
-        uint32_t* ubuf = cnt32 + (i >> 5) * kBuf;
-        const int r = i / kTW, w = i - r * kTW;
-        uint32_t V1 = 0, V2 = 0;
-        if (r + 1 < h_tile) {
-            const uint32_t t0 = tb[i], t1 = tb[i + kTW], S0 = S[i], S1 = S[i + kTW];
-            const uint32_t t1n = (w + 1 < kTW) ? tb[i + kTW + 1] : 0u;
-            const uint32_t S1n = (w + 1 < kTW) ? S[i + kTW + 1] : 0u;
-            const uint32_t t1s = (t1 >> 1) | (t1n << 31);   // bit x <- site x+1 of row r+1
-            const uint32_t S1s = (S1 >> 1) | (S1n << 31);
-            V1 = t0 & t1 & (S0 | S1);                        // (0,+1) union points
-            V2 = t0 & t1s & (S0 | S1s);                      // (+1,+1) union points
-        }
-        const uint32_t n = __popc(V1) + __popc(V2);
-        uint32_t incl = n;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-            if (lane >= o) incl += t;
-        }
-        const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-        for (uint32_t base = 0; base < total; base += kBuf) {
-            // entry = r << 9 | x << 1 | bond type, x = site column in the tile
-            uint32_t k = incl - n;
-            if (k < base + kBuf && k + n > base) {
-                for (uint32_t m = V1; m; m &= m - 1, ++k)
-                    if (k >= base && k < base + kBuf) ubuf[k - base] = (uint32_t)(r << 9) | ((32u * w + __ffs(m) - 1) << 1);
-                for (uint32_t m = V2; m; m &= m - 1, ++k)
-                    if (k >= base && k < base + kBuf)
-                        ubuf[k - base] = (uint32_t)(r << 9) | ((32u * w + __ffs(m) - 1) << 1) | 1u;
-            }
-            __syncwarp();
-            const uint32_t cnt_r = min(total - base, (uint32_t)kBuf);
-            for (uint32_t j = lane; j < cnt_r; j += 32) {
-                const uint32_t e = ubuf[j];
-                const int er = (int)(e >> 9), ex = (int)((e >> 1) & 255u);
-                union32(lab, run_start(S, C, er, ex), run_start(S, C, er + 1, ex + (int)(e & 1u)));
-            }
-            __syncwarp();
-        }
-    }
-    __syncthreads(); KK_CCLK(3)
-    for (int i = threadIdx.x; i < kTR * kTW; i += kThreads) {
-        const int base = (i / kTW) * kTX + 32 * (i % kTW);
-        for (uint32_t m = S[i]; m; m &= m - 1) cnt[base + __ffs(m) - 1] = 0;
-    }
-    __syncthreads(); KK_CCLK(4)
-    // sizes per root (one atomic per run segment) and edge-touch flags
-    for (int i = threadIdx.x; i < kTR * kTW; i += kThreads) {
-        const int r = i / kTW, w = i - r * kTW;
-        const bool edge_row = (r == 0 || r == h_tile - 1);
-        for (uint32_t m = tb[i]; m;) {
-            const uint64_t M = m, Lb = M & (~M + 1);
-            const uint32_t seg = (uint32_t)(((M + Lb) ^ M) & M);
-            m &= ~seg;
-            const int x0 = 32 * w + __ffs(seg) - 1;
-            const int x1 = 32 * w + 31 - __clz(seg);
-            const uint32_t root = root_of(lab, run_start(S, C, r, x0));
-            atomicAdd(&cnt32[root >> 1], (uint32_t)__popc(seg) << (16 * (root & 1)));
-            if (edge_row || x0 == 0 || x1 == w_tile - 1) atomicOr(&touch[root >> 5], 1u << (root & 31));
-        }
-    }
-    __syncthreads(); KK_CCLK(5)
-    // complete components -> histogram; edge components -> local node index
-    for (int i = threadIdx.x; i < kTR * kTW; i += kThreads) {
-        const int base = (i / kTW) * kTX + 32 * (i % kTW);
-        for (uint32_t m = S[i]; m; m &= m - 1) {
-            const uint32_t s0 = base + __ffs(m) - 1;
-            if (lab[s0] != s0) continue;
-            const uint32_t sz = cnt[s0];  // <= kSites fits 16 bits
-            if ((touch[s0 >> 5] >> (s0 & 31)) & 1u) {
-                const unsigned int k = atomicAdd(&n_nodes, 1u);
-                node_s[k] = (uint16_t)sz;
-                cnt[s0] = k;   // root -> local node index
-            } else if (sz < kSmallHist) {
-                atomicAdd(&shist[sz], 1u);
-            } else {
-                hist_add(P, rep, sz);
-            }
-        }
-    }
-    __syncthreads(); KK_CCLK(6)
-    for (int i = threadIdx.x; i < kSmallHist; i += kThreads)
-        if (shist[i]) atomicAdd(P.hist + rep * P.dense + i, shist[i]);
-    if (threadIdx.x == 0) node_base = atomicAdd(P.node_count, n_nodes);
-    __syncthreads(); KK_CCLK(7)
-    const unsigned int base = node_base;
-    for (unsigned int k = threadIdx.x; k < n_nodes; k += kThreads) {
-        if ((int64_t)(base + k) < P.node_cap) {
-            P.node_size[base + k] = node_s[k];
-            P.node_par[base + k] = base + k;
-            P.node_rep[base + k] = (uint32_t)rep;
-            P.root_size[base + k] = 0ull;
-        }
-    }
-    // edge export
-    const int64_t tile = (rep * P.tiles_y + ty) * P.tiles_x + tx;
-    uint32_t* E = P.edges + tile * kEdge;
-    for (int e = threadIdx.x; e < kEdge; e += kThreads) {
-        int r, x;
-        if (e < kTX) { r = 0; x = e; }                                   // top row
-        else if (e < 2 * kTX) { r = h_tile - 1; x = e - kTX; }           // bottom row
-        else if (e < 2 * kTX + kTR) { r = e - 2 * kTX; x = 0; }          // left column
-        else { r = e - 2 * kTX - kTR; x = w_tile - 1; }                  // right column
-        uint32_t v = kNone;
-        if (r < h_tile && x < w_tile && ((tb[r * kTW + (x >> 5)] >> (x & 31)) & 1u))
-            v = base + cnt[root_of(lab, run_start(S, C, r, x))];
-        E[e] = v;
-    }
-    KK_CCLK(8)
-}
-
-// ---- phase 1 (run-id variant, the default): union-find over compact run ids --
+// ---- phase 1: one CTA per tile, union-find over compact run ids ---------------
 // Runs get consecutive ids in row-major order: with B = the number of run
 // starts before a word (a CTA scan of popc(S)), the run containing target
 // site x (bit b of word w, row r) is
@@ -347,33 +149,61 @@ __global__ void __launch_bounds__(kThreads) ccl_tile_kernel(const CclParams P) {
 // atomic per warp and root.
 constexpr int kWords = kTR * kTW;
 constexpr int kMaxRuns = kSites / 2;
+static_assert(kMaxRuns <= 32768, "16-bit run ids and 16-bit component sizes");
 
 __device__ __forceinline__ uint32_t mask_le(int b) { return 0xFFFFFFFFu >> (31 - b); }
 
-// Union of the trees of nodes a and b (any members, e.g. a root found by an
+// Run parents are 32-bit (16-bit parents, a compiler-emitted CAS loop on the
+// containing word, measured slower at 128-row tiles: 18.2 vs 17.5 ms on
+// 65536^2); run / component sizes are 16-bit (<= kSites = 32768).
+typedef uint32_t run_t;
+
+__device__ __forceinline__ uint32_t run_find(run_t* par, uint32_t v) {
+    volatile run_t* vp = par;
+    uint32_t cur = vp[v];
+    while (cur != v) {
+        const uint32_t nxt = vp[cur];
+        if (nxt != cur) vp[v] = (run_t)nxt;
+        v = cur;
+        cur = nxt;
+    }
+    return v;
+}
+
+__device__ __forceinline__ uint32_t run_root(const run_t* par, uint32_t v) {
+    const volatile run_t* vp = par;
+    uint32_t cur = vp[v];
+    while (cur != v) {
+        v = cur;
+        cur = vp[v];
+    }
+    return v;
+}
+
+// Union of the trees of runs a and b (any members, e.g. a root found by an
 // earlier union): both walks interleaved (path splitting), then the larger
 // root is linked under the smaller by CAS.  Returns the surviving root.
-__device__ __forceinline__ uint32_t union_nodes(uint32_t* par, uint32_t a, uint32_t b) {
-    volatile uint32_t* vp = par;
+__device__ __forceinline__ uint32_t union_runs(run_t* par, uint32_t a, uint32_t b) {
+    volatile run_t* vp = par;
     for (;;) {
         uint32_t pa = vp[a], pb = vp[b];
         while (pa != a || pb != b) {
             if (pa != a) {
                 const uint32_t ga = vp[pa];
-                if (ga != pa) vp[a] = ga;
+                if (ga != pa) vp[a] = (run_t)ga;
                 a = pa;
                 pa = ga;
             }
             if (pb != b) {
                 const uint32_t gb = vp[pb];
-                if (gb != pb) vp[b] = gb;
+                if (gb != pb) vp[b] = (run_t)gb;
                 b = pb;
                 pb = gb;
             }
         }
         if (a == b) return a;
         const uint32_t hi = a > b ? a : b, lo = a > b ? b : a;
-        const uint32_t old = atomicCAS(par + hi, hi, lo);
+        const uint32_t old = atomicCAS(par + hi, (run_t)hi, (run_t)lo);
         if (old == hi) return lo;
         a = old;  // hi was linked meanwhile: continue from its new parent
         b = lo;
@@ -416,9 +246,11 @@ __global__ void __launch_bounds__(kThreads) ccl_runs_kernel(const CclParams P) {
     uint32_t* tb = smem;                   // [kWords] target bits
     uint32_t* S = tb + kWords;             // [kWords] run starts
     uint32_t* B = S + kWords;              // [kWords] runs started before the word
-    uint32_t* par = B + kWords;            // [kMaxRuns] union-find parent of each run
-    uint32_t* rsz = par + kMaxRuns;        // [kMaxRuns] run size; root: component size, then node index
-    uint32_t* touch = rsz + kMaxRuns;      // [kMaxRuns / 32] run / component touches the tile edge
+    constexpr int kParWords = kMaxRuns * (int)sizeof(run_t) / 4;
+    run_t* par = reinterpret_cast<run_t*>(B + kWords);  // [kMaxRuns] union-find parent of each run
+    uint32_t* rsz2 = B + kWords + kParWords;            // [kMaxRuns / 2] two 16-bit sizes per word:
+    unsigned short* rsz = reinterpret_cast<unsigned short*>(rsz2);  // run size; root: size, then node index
+    uint32_t* touch = rsz2 + kMaxRuns / 2;              // [kMaxRuns / 32] run / component touches the tile edge
     uint16_t* node_s = reinterpret_cast<uint16_t*>(touch + kMaxRuns / 32);  // [kEdge]
     __shared__ unsigned int n_nodes, node_base;
     __shared__ unsigned int wsum[kThreads / 32 + 1];
@@ -457,7 +289,7 @@ __global__ void __launch_bounds__(kThreads) ccl_runs_kernel(const CclParams P) {
     __syncthreads(); KK_CCLK(0)
     // ---- unions between rows r-1 and r (this thread's word is in row r).
     // The union points of the tile are listed in thread order (idc << 16 |
-    // ida, in the run-size array, unused until the next phase) and split into
+    // ida, in the run-size words, unused until the next phase) and split into
     // equal contiguous shares, so no warp waits for one with a dense row
     // block; consecutive points often share a run, whose root is reused.
     uint32_t U = 0, t0 = 0, s0 = 0, bb0 = 0;
@@ -474,20 +306,20 @@ __global__ void __launch_bounds__(kThreads) ccl_runs_kernel(const CclParams P) {
     uint32_t nu;
     uint32_t k = cta_excl_scan(__popc(U), wsum, nu);
     uint32_t last_c = 0xFFFFFFFFu, last_a = 0xFFFFFFFFu, root = 0;
-    if (nu <= (uint32_t)kMaxRuns) {
+    if (nu <= (uint32_t)(kMaxRuns / 2)) {
         while (U) {
             const int b = __ffs(U) - 1;
             U &= U - 1;
             const uint32_t m = mask_le(b);
             const uint32_t idc = b0 + __popc(st & m) - 1;
             const uint32_t ma = ((t0 >> b) & 1u) ? m : (m >> 1);
-            rsz[k++] = (idc << 16) | (bb0 + __popc(s0 & ma) - 1);
+            rsz2[k++] = (idc << 16) | (bb0 + __popc(s0 & ma) - 1);
         }
         __syncthreads();
         const uint32_t e1 = (uint32_t)(((uint64_t)nu * (i + 1)) / kThreads);
         for (uint32_t e = (uint32_t)(((uint64_t)nu * i) / kThreads); e < e1; ++e) {
-            const uint32_t pr = rsz[e], idc = pr >> 16, ida = pr & 0xFFFFu;
-            root = union_nodes(par, idc == last_c ? root : idc, ida == last_a ? root : ida);
+            const uint32_t pr = rsz2[e], idc = pr >> 16, ida = pr & 0xFFFFu;
+            root = union_runs(par, idc == last_c ? root : idc, ida == last_a ? root : ida);
             last_c = idc;
             last_a = ida;
         }
@@ -499,13 +331,13 @@ __global__ void __launch_bounds__(kThreads) ccl_runs_kernel(const CclParams P) {
             const uint32_t idc = b0 + __popc(st & m) - 1;
             const uint32_t ma = ((t0 >> b) & 1u) ? m : (m >> 1);
             const uint32_t ida = bb0 + __popc(s0 & ma) - 1;
-            root = union_nodes(par, idc == last_c ? root : idc, ida == last_a ? root : ida);
+            root = union_runs(par, idc == last_c ? root : idc, ida == last_a ? root : ida);
             last_c = idc;
             last_a = ida;
         }
     }
     __syncthreads();
-    for (uint32_t q = i; q < nr; q += kThreads) rsz[q] = 0u;
+    for (uint32_t q = i; q < (nr + 1) / 2; q += kThreads) rsz2[q] = 0u;
     __syncthreads();
     KK_CCLK(1)
     // ---- run sizes (per run segment of the word) and edge touches
@@ -518,16 +350,16 @@ __global__ void __launch_bounds__(kThreads) ccl_runs_kernel(const CclParams P) {
             const int xb0 = __ffs(seg) - 1;
             const int xb1 = 31 - __clz(seg);
             const uint32_t id = b0 + __popc(st & mask_le(xb0)) - 1;
-            atomicAdd(&rsz[id], (uint32_t)__popc(seg));
+            atomicAdd(&rsz2[id >> 1], (uint32_t)__popc(seg) << (16 * (id & 1)));
             if (edge_row || (w == 0 && xb0 == 0) || 32 * w + xb1 == w_tile - 1) atomicOr(&touch[id >> 5], 1u << (id & 31));
         }
     }
     __syncthreads(); KK_CCLK(2)
     // ---- component sizes and edge touches at the roots
     for (uint32_t k = i; k < nr; k += kThreads) {
-        const uint32_t root = find32(par, k);
+        const uint32_t root = run_find(par, k);
         if (root != k) {
-            atomicAdd(&rsz[root], rsz[k]);
+            atomicAdd(&rsz2[root >> 1], (uint32_t)rsz[k] << (16 * (root & 1)));
             if ((touch[k >> 5] >> (k & 31)) & 1u) atomicOr(&touch[root >> 5], 1u << (root & 31));
         }
     }
@@ -539,7 +371,7 @@ __global__ void __launch_bounds__(kThreads) ccl_runs_kernel(const CclParams P) {
         if ((touch[k >> 5] >> (k & 31)) & 1u) {
             const unsigned int n = atomicAdd(&n_nodes, 1u);
             node_s[n] = (uint16_t)sz;
-            rsz[k] = n;
+            rsz[k] = (unsigned short)n;
         } else if (sz < kSmallHist) {
             atomicAdd(&shist[sz], 1u);
         } else {
@@ -574,7 +406,7 @@ __global__ void __launch_bounds__(kThreads) ccl_runs_kernel(const CclParams P) {
             const int wi = er * kTW + (ex >> 5);
             if ((tb[wi] >> (ex & 31)) & 1u) {
                 const uint32_t id = B[wi] + __popc(S[wi] & mask_le(ex & 31)) - 1;
-                val = base + rsz[root_of(par, id)];
+                val = base + rsz[run_root(par, id)];
             }
         }
         E[e] = val;
@@ -775,10 +607,6 @@ cudaError_t launch_ccl(const uint32_t* lat, const Geom& g, int64_t replicas, int
                        unsigned long long* root_size, unsigned int* counter, unsigned int* hist, int64_t dense,
                        unsigned long long* big, unsigned long long* nbig, int64_t big_cap, cudaStream_t s,
                        const SlabCclArgs* slab) {
-    static const bool ccl_old_tiles = [] {
-        const char* v = std::getenv("KK_CCL_OLD");
-        return v && *v == '1';
-    }();
     CclParams P{};
     P.periodic_y = slab ? 0 : 1;
     if (slab) {
@@ -807,17 +635,10 @@ cudaError_t launch_ccl(const uint32_t* lat, const Geom& g, int64_t replicas, int
     P.node_cap = ccl_node_cap(g, replicas);
     cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(unsigned int), s);
     if (e != cudaSuccess) return e;
-    if (ccl_old_tiles) {
-        const int smem = 4 * (2 * kTR * kTW + kSites / 32 + kSites + kSites / 2 + kEdge / 2 + kTR * kTW);
-        e = ensure_dynamic_smem((const void*)ccl_tile_kernel, smem);
-        if (e != cudaSuccess) return e;
-        ccl_tile_kernel<<<dim3(P.tiles_x, P.tiles_y, (unsigned)replicas), kThreads, smem, s>>>(P);
-    } else {
-        const int smem = 4 * (3 * kWords + 2 * kMaxRuns + kMaxRuns / 32 + kEdge / 2);
-        e = ensure_dynamic_smem((const void*)ccl_runs_kernel, smem);
-        if (e != cudaSuccess) return e;
-        ccl_runs_kernel<<<dim3(P.tiles_x, P.tiles_y, (unsigned)replicas), kThreads, smem, s>>>(P);
-    }
+    const int smem = 4 * (3 * kWords + kMaxRuns * (int)sizeof(run_t) / 4 + kMaxRuns / 2 + kMaxRuns / 32 + kEdge / 2);
+    e = ensure_dynamic_smem((const void*)ccl_runs_kernel, smem);
+    if (e != cudaSuccess) return e;
+    ccl_runs_kernel<<<dim3(P.tiles_x, P.tiles_y, (unsigned)replicas), kThreads, smem, s>>>(P);
     count_launch();
     const int64_t per_rep = (int64_t)P.tiles_x * P.tiles_y * (kTR + kTX);
     int bx = grid_for_n(per_rep);

@@ -1,8 +1,7 @@
 """Phase clocks of the CCL tile kernel (library built with -DKK_CCL_CLK):
 KK_LIB=paper_1309_4349_b200/libkk_cclclk.so python tools/ccl_clocks.py [L] [sweeps]
 Phases of ccl_runs_kernel: load + run ids, unions, run sizes, root sizes,
-roots -> hist/nodes, node + edge export (KK_CCL_OLD=1: the previous tile
-kernel's phases); thread 0 of every CTA, summed."""
+roots -> hist/nodes, node + edge export; thread 0 of every CTA, summed."""
 import ctypes
 import os
 import sys
@@ -25,11 +24,7 @@ lib.kk_debug_ccl_clocks(buf)
 lat.cluster_histogram(1)
 torch.cuda.synchronize()
 lib.kk_debug_ccl_clocks(buf)
-if os.environ.get("KK_CCL_OLD") == "1":
-    names = ["load", "run starts", "carry", "unions", "zero sizes", "sizes", "roots->hist/nodes", "node base",
-             "node+edge export"]
-else:  # ccl_runs_kernel
-    names = ["load + run ids", "unions", "run sizes", "root sizes", "roots->hist/nodes", "node+edge export"]
+names = ["load + run ids", "unions", "run sizes", "root sizes", "roots->hist/nodes", "node+edge export"]
 tot = sum(buf[k] for k in range(len(names)))
 for k, nm in enumerate(names):
     print(f"{nm:20s} {buf[k] / tot:6.3f}")
