@@ -23,9 +23,10 @@
 //     split as 6 w = d 2^32 + u into the direction d and the acceptance
 //     uniform u (one 32x32->64 multiply);
 //   * acceptance (R5): a move with v on the favourable side (dE <= 0) is
-//     accepted without a draw; the others need u <= thr[|v|].  Every uniform
-//     is compared with the three thresholds as soon as it is drawn; each
-//     centre's |v| picks its result.  (Comparing only the uniforms that are
+//     accepted without a draw; the others need u <= thr[|v|].  Each uniform's
+//     level against the three (ordered) thresholds is found as soon as it is
+//     drawn, in two compares (u <= t2, then u <= t3 or t1); each centre's |v|
+//     picks its result.  (Comparing only the uniforms that are
 //     needed, through a warp-compacted queue, cost more than it saved: ~70%
 //     of the calls are needed.)
 // Flips are XOR masks per plane word (shared-memory atomics: centres are 4
@@ -146,6 +147,21 @@ __device__ __forceinline__ uint32_t wrap_group(int gm, int Wg) {
 }
 
 __device__ __forceinline__ uint32_t mux(uint32_t s, uint32_t a1, uint32_t a0) { return (a1 & s) | (a0 & ~s); }
+
+// Acceptance level of a uniform in two compares (t1 >= t2 >= t3, R5): bit of
+// e1 = [u <= t2], bit of e0 = [u <= (u <= t2 ? t3 : t1)]; then u <= t1 is
+// e1 | e0, u <= t2 is e1, u <= t3 is e1 & e0.
+__device__ __forceinline__ void level_bits(uint32_t& e1, uint32_t& e0, uint32_t u, uint32_t t1, uint32_t t2,
+                                           uint32_t t3, uint32_t bit) {
+    asm("{\n\t.reg .pred p, q;\n\t.reg .b32 t;\n\t"
+        "setp.le.u32 p, %2, %4;\n\t"
+        "selp.b32 t, %5, %3, p;\n\t"
+        "setp.le.u32 q, %2, t;\n\t"
+        "@p or.b32 %0, %0, %6;\n\t"
+        "@q or.b32 %1, %1, %6;\n\t}"
+        : "+r"(e1), "+r"(e0)
+        : "r"(u), "r"(t1), "r"(t2), "r"(t3), "r"(bit));
+}
 __device__ __forceinline__ uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) { return (a & b) | (c & (a | b)); }
 
 // Items of one iteration (class KX, centre rows r_first + 4a, a < nrows), all
@@ -171,12 +187,13 @@ __device__ __forceinline__ void pl_iteration(const PlCtx& X, uint32_t* tile, con
             Mg = gt[m];
             // ---- draws (R6): call c = 8 Mg + q (q = 0..7, octet g = 4 Mg + (q >> 1))
             // holds the words of centres 4q..4q+3; 6 w = d 2^32 + u gives the
-            // direction d and the acceptance uniform u.  Every uniform is tested
-            // against the thresholds of |v| = 1, 2, 3 here (R5: L1..L3), before
-            // the energy change is known; each centre's |v| picks its result
+            // direction d and the acceptance uniform u.  Every uniform's
+            // acceptance level against the thresholds of |v| = 1, 2, 3 (R5) is
+            // found here in two compares (bit planes E1, E0), before the
+            // energy change is known; each centre's |v| picks its result
             // below.  Four directions per table lookup (entry (6 d0 + d1) * 36 +
             // 6 d2 + d3), transposed into the bit planes D0..D2.
-            uint32_t L1 = 0, L2 = 0, L3 = 0;
+            uint32_t E1 = 0, E0 = 0;
             uint32_t f[4];
 #pragma unroll
             for (int bt = 0; bt < 2; ++bt) {
@@ -194,9 +211,7 @@ __device__ __forceinline__ void pl_iteration(const PlCtx& X, uint32_t* tile, con
                         d[i] = (uint32_t)(pr >> 32);
                         const uint32_t u = (uint32_t)pr;
                         const uint32_t bit = 1u << (16 * bt + 4 * qd + i);
-                        L1 = or_if_le(L1, u, X.t1, bit);
-                        L2 = or_if_le(L2, u, X.t2, bit);
-                        L3 = or_if_le(L3, u, X.t3, bit);
+                        level_bits(E1, E0, u, X.t1, X.t2, X.t3, bit);
                     }
                     e[qd] = dt[((d[0] * 6u + d[1]) * 6u + d[2]) * 6u + d[3]];
                 }
@@ -280,7 +295,7 @@ __device__ __forceinline__ void pl_iteration(const PlCtx& X, uint32_t* tile, con
             need = nontriv & mux(X.mdn, dn, up) & X.mall;
             autoacc = nontriv & ~need;
             // accepted with a draw: u <= thr[|v|] (R5)
-            drawn = need & mux(M1, mux(M0, L3, L2), L1);
+            drawn = need & mux(M1, mux(M0, E1 & E0, E1), E1 | E0);
         }
         if (has) {
             // accepted: every favourable move, and the drawn ones with u32 <= thr[|v|]
