@@ -49,6 +49,45 @@ __device__ __forceinline__ void philox10_xn(const uint32_t m[N], uint32_t c1, ui
     }
 }
 
+// As philox10_xn<4> for the counters c0, c0+1, c0+2, c0+3: the first round's
+// products M0 (c0 + p) = M0 c0 + M0 p take one widening multiply and three
+// 64-bit adds of constants (the other rounds are unchanged).
+__device__ __forceinline__ void philox10_x4_consec(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                                   const uint32_t* rk, uint32_t out[4][4]) {
+    uint32_t a[4], b[4], c[4], d[4];
+    const uint64_t base = (uint64_t)kPhiloxM0 * c0;
+    const uint64_t p1 = (uint64_t)kPhiloxM1 * c2;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+        const uint64_t p0 = base + (uint64_t)kPhiloxM0 * (uint64_t)p;
+        a[p] = (uint32_t)(p1 >> 32) ^ c1 ^ rk[0];
+        b[p] = (uint32_t)p1;
+        c[p] = (uint32_t)(p0 >> 32) ^ c3 ^ rk[10];
+        d[p] = (uint32_t)p0;
+    }
+#pragma unroll
+    for (int round = 1; round < 10; ++round) {
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            const uint64_t q0 = (uint64_t)kPhiloxM0 * a[p];
+            const uint64_t q1 = (uint64_t)kPhiloxM1 * c[p];
+            const uint32_t na = (uint32_t)(q1 >> 32) ^ b[p] ^ rk[round];
+            const uint32_t nc = (uint32_t)(q0 >> 32) ^ d[p] ^ rk[10 + round];
+            b[p] = (uint32_t)q1;
+            d[p] = (uint32_t)q0;
+            a[p] = na;
+            c[p] = nc;
+        }
+    }
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+        out[p][0] = a[p];
+        out[p][1] = b[p];
+        out[p][2] = c[p];
+        out[p][3] = d[p];
+    }
+}
+
 // As philox10_xn with a counter word 1 per stream.
 template <int N>
 __device__ __forceinline__ void philox10_xnc(const uint32_t m[N], const uint32_t c1[N], uint32_t c2, uint32_t c3,
