@@ -48,6 +48,18 @@ def test_bench_lattice_plan(monkeypatch):
     monkeypatch.delenv("KK_PLANAR")
 
 
+def test_planar_cost_model_picks_the_measured_shapes():
+    """The refitted planar cost model (halo groups weighted; 512-thread CTAs
+    for one-wave grids with <= 512 items per iteration) reproduces the shapes
+    measured fastest on a B200 after the R6 revision (planar
+    kernel: 4096^2 64 x 56 at 512 threads 352 vs 32 x 112 326 G/s; 8192^2
+    128 x 112 574 vs 64 x 224 555; 16384^2 128 x 224 666; 65536^2 128 x 340)."""
+    want = {4096: (64, 56, 512), 8192: (128, 112, 768), 16384: (128, 224, 768), 65536: (128, 340, 768)}
+    for L, (twi, thi, nt) in want.items():
+        p = kk.plan(L, L, n_sm=148)
+        assert (p["kernel"], p["tile_words"], p["tile_rows"], p["threads"]) == ("planar", twi, thi, nt), (L, p)
+
+
 def test_mid_size_lattice_fills_every_sm(monkeypatch):
     p = kk.plan(4096, 4096)
     assert p["kernel"] == "planar" and p["ctas"] >= 128
