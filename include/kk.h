@@ -114,16 +114,20 @@ int kk_destroy(kk_handle h);
  * handle's sweep counter (and iteration, if kk_pass left it mid-sweep).  Only
  * for full-lattice handles (KK_ERR_STATE on a slab).  Asynchronous on
  * `stream`.  The kernel is chosen at kk_create time and never changes the
- * result (every path is bit-identical): replicas that fit in one
- * SM's shared memory run the resident kernel (all n sweeps in one launch),
- * larger lattices the tile kernel (16/T launches per sweep);
- * environment overrides for testing: KK_RESIDENT=0/2 (never/always when it
- * fits), KK_BAND=2 (band kernel), KK_THI/KK_TWI (tile shape),
- * KK_RES_THREADS=128/256/512, KK_PASS_THREADS=384/512/640 (640: T = 8), KK_TMA=0 (LDG
- * instead of TMA staging), KK_PDL=0/1 (programmatic dependent launch of
- * consecutive tile-kernel passes; default: when the grid fits the GPU at
- * once), KK_CLUSTER=2/4/8/16 (cluster kernel: the band
- * kernel inside one thread-block cluster per replica, halos over DSMEM). */
+ * result (every path is bit-identical): replica batches whose
+ * replicas fit in one SM's shared memory run the resident kernel (all n
+ * sweeps in one launch), one or a few mid-small lattices the cluster kernel
+ * (one thread-block cluster per replica, DSMEM halos), lattices with
+ * Lx % 128 == 0 from 2^24 sites the planar tile kernel and other large
+ * lattices the row-major tile kernel (16/T launches per sweep) or, >= 8192
+ * wide, the band kernel; kk_plan_config reports the choice.  Environment
+ * overrides for testing: KK_RESIDENT=0/2 (never/always when it fits),
+ * KK_PLANAR=0/2 (never/whenever the rows allow), KK_BAND=0/2, KK_CLUSTER=0 or
+ * 2/4/8/16 (cluster size), KK_THI/KK_TWI (tile shape), KK_RES_THREADS=
+ * 128/256/512, KK_PASS_THREADS (row-major 384/512/640, planar
+ * 512/640/768/896), KK_TMA=0 (LDG instead of TMA staging), KK_PDL=0/1
+ * (programmatic dependent launch of consecutive passes; default: when the
+ * grid fits the GPU at once). */
 int kk_sweep(kk_handle h, int64_t n, void* stream);
 
 /* Energy per replica (R3): nab_out[r] = N_AB (unlike nearest-neighbour pairs,
