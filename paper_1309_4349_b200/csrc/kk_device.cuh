@@ -88,41 +88,6 @@ __device__ __forceinline__ void philox10_x4_consec(uint32_t c0, uint32_t c1, uin
     }
 }
 
-// As philox10_xn with a counter word 1 per stream.
-template <int N>
-__device__ __forceinline__ void philox10_xnc(const uint32_t m[N], const uint32_t c1[N], uint32_t c2, uint32_t c3,
-                                             const uint32_t* rk, uint32_t out[N][4]) {
-    uint32_t a[N], b[N], c[N], d[N];
-#pragma unroll
-    for (int p = 0; p < N; ++p) {
-        a[p] = m[p];
-        b[p] = c1[p];
-        c[p] = c2;
-        d[p] = c3;
-    }
-#pragma unroll
-    for (int round = 0; round < 10; ++round) {
-#pragma unroll
-        for (int p = 0; p < N; ++p) {
-            const uint64_t p0 = (uint64_t)kPhiloxM0 * a[p];
-            const uint64_t p1 = (uint64_t)kPhiloxM1 * c[p];
-            const uint32_t na = (uint32_t)(p1 >> 32) ^ b[p] ^ rk[round];
-            const uint32_t nc = (uint32_t)(p0 >> 32) ^ d[p] ^ rk[10 + round];
-            b[p] = (uint32_t)p1;
-            d[p] = (uint32_t)p0;
-            a[p] = na;
-            c[p] = nc;
-        }
-    }
-#pragma unroll
-    for (int p = 0; p < N; ++p) {
-        out[p][0] = a[p];
-        out[p][1] = b[p];
-        out[p][2] = c[p];
-        out[p][3] = d[p];
-    }
-}
-
 // acc | bit if u <= t: a compare and a predicated OR (the compiler's own
 // select + add form costs a third more ALU-pipe instructions).
 __device__ __forceinline__ uint32_t or_if_le(uint32_t acc, uint32_t u, uint32_t t, uint32_t bit) {
